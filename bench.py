@@ -1,0 +1,438 @@
+"""Benchmark: MoE dispatch+combine (Fusco shuffle) on 1-8 B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl fusco|reference]
+
+N > 1 is launched by torchrun (one process per GPU, NCCL bootstrap only).
+A step = one pass of the hot path over one batch: on-device layout planner
+(fs_layout) + dispatch (fs_dispatch) + combine (fs_combine), identity expert
+(combine pulls the dispatched rows straight back), fp32 accumulation, bf16
+payloads.  Inputs are resident in HBM for ``value``; ``e2e`` repeats the
+step through the public API with pinned host buffers and the H2D/D2H copies
+inside the timed region.  ``--impl reference`` times the reference CPU path
+(the oracle port, threaded numpy) on the host cores instead.
+
+Unit of ``value``: GB/s of routed rows = Σ_ranks 2·T_l·K·token_bytes (the
+rows dispatch delivers plus the rows combine reduces) ÷ step time, whole job.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = json.loads((ROOT / "BASELINE.json").read_text())["metric"] if (ROOT / "BASELINE.json").exists() else \
+    "MoE dispatch+combine latency (us) and GB/s/GPU vs NVLink peak, 1-8 B200"
+
+CONFIGS = {
+    # name: hidden, dtype, experts, topk, tokens/rank, zipf_s, description
+    "oracle": (1024, "f32", 8, 2, 4096, 0.0,
+               "synthetic oracle case: hidden 1024 fp32, 8 experts top-2, 4096 tokens/rank, uniform"),
+    "mixtral": (4096, "bf16", 8, 2, 8192, 0.0,
+                "Mixtral-8x7B shape: hidden 4096 bf16, 8 experts top-2, 8192 tokens/rank, uniform, EP=N"),
+    "qwen3": (2048, "bf16", 128, 8, 4096, 0.0,
+              "Qwen3-30B-A3B shape: hidden 2048 bf16, 128 experts top-8, 4096 tokens/rank, EP=N"),
+    "dsv3": (7168, "bf16", 256, 8, 4096, 0.0,
+             "DeepSeek-V3 shape: hidden 7168 bf16, 256 experts top-8, 4096 tokens/rank, per-rank dedup, EP=N"),
+    "dsv3_decode": (7168, "bf16", 256, 8, 128, 0.0,
+                    "DeepSeek-V3 decode batch: hidden 7168 bf16, 256 experts top-8, 128 tokens/rank, EP=N"),
+    "dsv3_zipf": (7168, "bf16", 256, 8, 4096, 1.2,
+                  "DeepSeek-V3 shape under Zipf s=1.2 routing, 4096 tokens/rank, EP=N"),
+}
+DEFAULT_CONFIG = "mixtral"  # BASELINE.json configs[1]
+
+NVLINK_NOMINAL = 900.0   # GB/s per direction per GPU (NVLink 5)
+NVLINK_MEASURED = 770.0  # GB/s peer copy, B200_PROFILING.md
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm": float(d["hbm_gbs"]), "hbm_src": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm": 6650.0, "hbm_src": "fallback (B200_PROFILING.md)"}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes (host numpy over the routing metadata)
+
+
+def traffic(experts: np.ndarray, source: np.ndarray, owner: np.ndarray, P: int, tb: int, T_l: int) -> dict:
+    own = owner[experts]
+    K = experts.shape[1]
+    first = np.ones(own.shape, dtype=bool)
+    for k in range(1, K):
+        first[:, k] = (own[:, :k] != own[:, k : k + 1]).all(axis=1)
+    remote = own != source[:, None]
+    send = first & remote
+    d_eg = np.bincount(source, weights=send.sum(1), minlength=P) * tb
+    d_in = np.bincount(own[send], minlength=P) * tb
+    c_eg = np.bincount(own[remote], minlength=P) * tb          # rows pulled out of owner g
+    c_in = np.bincount(source, weights=remote.sum(1), minlength=P) * tb
+    rows = np.bincount(own.reshape(-1), minlength=P)
+    # HBM bytes of each kernel on each rank (reads + writes of payload rows)
+    dedup_rows_in = np.bincount(own[send], minlength=P)
+    hbm_disp = T_l * tb + rows * tb + (rows - dedup_rows_in) * tb * (P > 1)  # read x, write rows (+fan-out read)
+    hbm_comb = rows * tb + T_l * tb
+    return dict(d_eg=d_eg, d_in=d_in, c_eg=c_eg, c_in=c_in, rows=rows, hbm_disp=hbm_disp, hbm_comb=hbm_comb)
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-i", str(index),
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def stop(self) -> dict | None:
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+
+
+def parse():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="fusco", choices=["fusco", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--soak-s", type=float, default=1.5, help="untimed load before timing (clock ramp, sampling)")
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+def routing_for(cfg_name: str, P: int, seed: int):
+    from paper_2512_22036_b200 import box, gen_realworld, round_robin_placement
+
+    hidden, dtype, E, K, T_l, zipf, desc = CONFIGS[cfg_name]
+    topo = box(P)
+    pl = round_robin_placement(E, topo)
+    a = gen_realworld(P * T_l, K, topo, pl, seed=seed, zipf_s=zipf)
+    return a, pl
+
+
+def cpu_reference(cfg_name: str, P: int, seed: int, steps: int, warmup: int, budget_s: float = 150.0):
+    """Reference CPU path (oracle port) on a bounded sample of the workload."""
+    from oracle.cpu_baseline import shuffle_times
+
+    hidden, dtype, E, K, T_l, zipf, desc = CONFIGS[cfg_name]
+    a, pl = routing_for(cfg_name, P, seed)
+    elem = 2 if dtype == "bf16" else 4
+    tb = hidden * elem
+    rng = np.random.default_rng(seed + 1)
+    T = a.num_tokens
+
+    def run(n_tok):
+        sel = np.arange(n_tok)  # first n_tok global tokens: a balanced slice of every rank
+        pay = rng.integers(0, 256, size=(n_tok, tb), dtype=np.uint8)
+        if dtype == "bf16":  # keep values finite: random sign/exponent-safe bf16 bit patterns
+            pay.view(np.uint16)[:] = (pay.view(np.uint16) & 0x3FFF) | 0x3000
+        else:
+            pay.view(np.float32)[:] = rng.standard_normal((n_tok, tb // 4)).astype(np.float32)
+        t = shuffle_times(a.experts[sel], a.weights[sel], a.source[sel], pl.owner, P, pay, dtype)
+        return t, 2 * n_tok * K * tb
+
+    # calibrate the sample so warmup+steps fit the budget
+    n = min(T, 256)
+    (tp, td, tc, thr), _ = run(n)
+    per_tok = max((tp + td + tc) / n, 1e-7)
+    n = int(min(T, max(64, budget_s / max(1, steps + warmup) / per_tok)))
+    vals, lat = [], []
+    for i in range(warmup + steps):
+        (tp, td, tc, thr), nbytes = run(n)
+        if i >= warmup:
+            vals.append(nbytes / (tp + td + tc) / 1e9)
+            lat.append(tp + td + tc)
+    return {
+        "value": float(np.median(vals)),
+        "unit": "GB/s",
+        "cores": int(thr),
+        "kind": "port",
+        "sample": f"{n} of {T} tokens of the same routing (first {n} global ids, all {P} ranks), "
+                  f"plan+dispatch+combine, median of {steps} runs; host os.cpu_count()={os.cpu_count()}",
+        "latency_s": float(np.median(lat)),
+    }
+
+
+def main() -> int:
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        args.gpus = world
+    hidden, dtype, E, K, T_l, zipf, desc = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        cb = cpu_reference(args.config, world, args.seed, args.steps, args.warmup)
+        line = {
+            "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": cb["unit"], "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["latency_s"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+            "data": "synthetic", "config": {"workload": desc, "ep": world},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_22036_b200 import EPBuffer
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    P = world
+    a, pl = routing_for(args.config, P, args.seed)
+    elem = 2 if dtype == "bf16" else 4
+    tb = hidden * elem
+    tr = traffic(a.experts, a.source, pl.owner, P, tb, T_l)
+    ids = np.flatnonzero(a.source == rank)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+
+    buf = EPBuffer(num_experts=E, topk=K, hidden=hidden, dtype=dtype, max_tokens=T_l, with_act_out=False)
+    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+    NSET = 2  # rotate input/output sets so consecutive steps touch different memory (L2 126 MB)
+    xs = [torch.randn(T_l, hidden, device=dev, generator=gen).to(tdt) for _ in range(NSET)]
+    outs = [torch.empty(T_l, hidden, device=dev, dtype=tdt) for _ in range(NSET)]
+    idx = torch.as_tensor(a.experts[ids], device=dev).contiguous()
+    w = torch.as_tensor(a.weights[ids], dtype=torch.float32, device=dev).contiguous()
+    plan = buf.r.new_plan(idx, with_masks=False)
+    r = buf.r
+    from paper_2512_22036_b200._lib import FS_PHASE_ALL, FS_SRC_ACT
+
+    def step(j, ev=None):
+        if ev is not None:
+            ev[0].record()
+        r.layout(plan, FS_PHASE_ALL)
+        if ev is not None:
+            ev[1].record()
+        r.dispatch(xs[j % NSET], plan, FS_PHASE_ALL)
+        if ev is not None:
+            ev[2].record()
+        r.combine(plan, w, outs[j % NSET], dtype_code=buf.dtype_code, src=FS_SRC_ACT, acc=0, phase=FS_PHASE_ALL)
+        if ev is not None:
+            ev[3].record()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # correctness guard before timing (cheap): a round trip must reproduce x (weights sum to 1)
+    step(0)
+    buf.check()
+    rt = (xs[0].float() * w.sum(1, keepdim=True)).to(tdt).float()
+    if not torch.allclose(outs[0].float(), rt, rtol=2.0**-7, atol=2e-2):
+        raise SystemExit("bench: round-trip check failed")
+
+    sampler = ClockSampler(local)
+    for i in range(args.warmup):
+        step(i)
+    barrier()
+    t_end = time.time() + args.soak_s
+    j = 0
+    while time.time() < t_end:
+        for _ in range(20):
+            step(j)
+            j += 1
+        torch.cuda.synchronize()
+    barrier()
+
+    # ---- timed region: EXACTLY K steps, device time, max over ranks --------
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    start.record()
+    for i in range(args.steps):
+        step(i, evs[i])
+    end.record()
+    barrier()
+    buf.check()
+    total_ms = start.elapsed_time(end)
+    k_layout = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    k_disp = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    k_comb = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
+    launches = 3 * args.steps
+
+    # ---- e2e: public API, pinned host buffers, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        xh = [x.cpu().pin_memory() for x in xs]
+        oh = [torch.empty(T_l, hidden, dtype=tdt).pin_memory() for _ in range(NSET)]
+        idx_h = torch.as_tensor(a.experts[ids]).pin_memory()
+        w_h = torch.as_tensor(a.weights[ids], dtype=torch.float32).pin_memory()
+        xd = [torch.empty_like(xs[0]) for _ in range(NSET)]
+        idx_d = torch.empty_like(idx)
+        w_d = torch.empty_like(w)
+
+        def e2e_step(j):
+            xd[j % NSET].copy_(xh[j % NSET], non_blocking=True)
+            idx_d.copy_(idx_h, non_blocking=True)
+            w_d.copy_(w_h, non_blocking=True)
+            p = buf.build_plan(idx_d)
+            buf.dispatch(xd[j % NSET], p)
+            o = buf.combine(p, w_d, src="act")
+            oh[j % NSET].copy_(o, non_blocking=True)
+
+        for i in range(max(3, args.warmup // 4)):
+            e2e_step(i)
+        barrier()
+        s2, t2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s2.record()
+        for i in range(args.steps):
+            e2e_step(i)
+        t2.record()
+        barrier()
+        e2e_ms = s2.elapsed_time(t2)
+        h2d = T_l * tb + T_l * K * 8 + T_l * K * 4
+        e2e = {"ms": e2e_ms, "h2d": h2d, "d2h": T_l * tb}
+    clocks = sampler.stop()
+
+    vec = torch.tensor([total_ms, k_layout, k_disp, k_comb, e2e["ms"] if e2e else 0.0], dtype=torch.float64,
+                       device=dev)
+    if world > 1:
+        dist.all_reduce(vec, op=dist.ReduceOp.MAX)
+    total_ms, k_layout, k_disp, k_comb, e2e_ms = vec.tolist()
+    ms = total_ms / args.steps
+    routed = 2.0 * P * T_l * K * tb  # bytes per step, whole job
+    value = routed / (ms * 1e-3) / 1e9
+
+    pk = peaks()
+    if P == 1:
+        disp_b, comb_b = float(tr["hbm_disp"][0]), float(tr["hbm_comb"][0])
+        t_min_d, t_min_c = disp_b / (pk["hbm"] * 1e9), comb_b / (pk["hbm"] * 1e9)
+        dom = "fs_dispatch" if k_disp >= k_comb else "fs_combine"
+        b, t = (disp_b, k_disp) if dom == "fs_dispatch" else (comb_b, k_comb)
+        achieved = b / (t * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk["hbm"], "unit": "GB/s",
+                "frac": achieved / pk["hbm"], "peak_src": pk["hbm_src"], "bytes_per_launch": b,
+                "traffic": None}
+    else:
+        d_bn = float(np.maximum(tr["d_eg"], tr["d_in"]).max())
+        c_bn = float(np.maximum(tr["c_eg"], tr["c_in"]).max())
+        t_min_d, t_min_c = d_bn / (NVLINK_NOMINAL * 1e9), c_bn / (NVLINK_NOMINAL * 1e9)
+        dom = "fs_dispatch" if k_disp >= k_comb else "fs_combine"
+        b, t = (d_bn, k_disp) if dom == "fs_dispatch" else (c_bn, k_comb)
+        achieved = b / (t * 1e-3) / 1e9
+        roof = {"bound": "nvlink", "kernel": dom, "achieved": achieved, "peak": NVLINK_MEASURED, "unit": "GB/s",
+                "frac": achieved / NVLINK_MEASURED, "peak_src": "measured peer copy 770 GB/s/dir (B200_PROFILING.md)",
+                "frac_of_nominal_900": achieved / NVLINK_NOMINAL,
+                "bytes_per_launch": b, "traffic": None}
+    traffic_file = ROOT / "profiles" / "ncu_traffic.json"
+    if traffic_file.exists():
+        tf = json.loads(traffic_file.read_text())
+        roof["traffic"] = tf.get(f"{args.config}/n{P}/{dom}")
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "GB/s",
+        "n_gpus": P,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": dtype,
+        "data": "synthetic: reference gen_realworld routing (seed 0) + random payload rows",
+        "config": {
+            "workload": desc,
+            "ep": P,
+            "tokens_per_rank": T_l,
+            "hidden": hidden,
+            "experts": E,
+            "topk": K,
+            "zipf_s": zipf,
+            "expert": "identity (combine pulls the dispatched rows)",
+            "combine_accumulate": "fp32",
+            "l2": f"inputs larger than L2: {NSET} rotating input/output sets + double-buffered activations, "
+                  f"{(T_l * tb * 2 + int(tr['rows'].max()) * tb) / 2**20:.0f} MiB touched per step per rank",
+            "value_def": "routed-row bytes (dispatch + combine, all ranks) / step time",
+        },
+        "latency_us": ms * 1e3,
+        "kernel_us": {"fs_layout": k_layout * 1e3, "fs_dispatch": k_disp * 1e3, "fs_combine": k_comb * 1e3},
+        "t_min_us": {"fs_dispatch": t_min_d * 1e6, "fs_combine": t_min_c * 1e6},
+        "roofline_step_frac": (t_min_d + t_min_c) / (ms * 1e-3),
+        "nvlink_gbps_per_gpu": None if P == 1 else {
+            "dispatch": float(tr["d_eg"].mean()) / (k_disp * 1e-3) / 1e9,
+            "combine": float(tr["c_eg"].mean()) / (k_comb * 1e-3) / 1e9,
+        },
+        "roofline": roof,
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if e2e is not None:
+        line["e2e"] = {"value": routed / (e2e_ms / args.steps * 1e-3) / 1e9, "unit": "GB/s",
+                       "ms_per_step": e2e_ms / args.steps, "h2d_bytes_per_step": e2e["h2d"] * P,
+                       "d2h_bytes_per_step": e2e["d2h"] * P}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_reference(args.config, 1, args.seed, steps=3, warmup=1, budget_s=25.0)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    buf.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

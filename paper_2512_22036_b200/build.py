@@ -1,0 +1,74 @@
+"""Build libfusco.so in-tree with nvcc for sm_100a (B200) only.
+
+The shared library is the C-ABI boundary declared in include/fusco.h; it is
+written next to this file (``lib/libfusco.so``) so it travels with the repo
+snapshot to the GPU box.  nvcc cross-compiles here without a GPU.
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB_DIR = PKG / "lib"
+LIB = LIB_DIR / "libfusco.so"
+SOURCES = [CSRC / "fusco.cu"]
+DEPS = SOURCES + [CSRC / "fusco_kernels.cuh", CSRC / "fusco_device.cuh", ROOT / "include" / "fusco.h"]
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nvcc_path() -> str:
+    cand = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not Path(cand).exists():
+        raise RuntimeError("nvcc not found; the CUDA toolkit is required to build libfusco")
+    return cand
+
+
+def needs_build() -> bool:
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    return any(p.stat().st_mtime > t for p in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not needs_build():
+        return LIB
+    LIB_DIR.mkdir(exist_ok=True)
+    tmp = LIB.with_suffix(".so.tmp")
+    cmd = [
+        nvcc_path(),
+        *ARCH,
+        "-O3",
+        "-lineinfo",
+        "-std=c++17",
+        "-shared",
+        "-Xcompiler",
+        "-fPIC,-O2",
+        "-Xptxas",
+        "-v" if verbose else "-O3",
+        "-I",
+        str(ROOT / "include"),
+        "-o",
+        str(tmp),
+        *map(str, SOURCES),
+    ]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if verbose or res.returncode:
+        sys.stderr.write(res.stdout + res.stderr)
+    if res.returncode:
+        raise RuntimeError(f"nvcc failed ({res.returncode}): {' '.join(cmd)}")
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

@@ -1,0 +1,445 @@
+// fusco.cu — libfusco.so: the extern "C" boundary (include/fusco.h) around
+// the sm_100a shuffle kernels.  Host code here only validates, keeps the
+// per-rank handle, and launches; it never touches payload bytes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fusco_kernels.cuh"
+
+using namespace fusco;
+
+namespace {
+
+constexpr int kMaxCtasPerSm = 4;
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define FS_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return fail(FS_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e));        \
+  } while (0)
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct RegionLayout {
+  size_t off_count, count_stride, off_fansrc, fansrc_stride, off_act, act_stride, off_actout, total;
+};
+
+RegionLayout region_layout(int world, int E, int tb, long long max_rows, int with_act_out) {
+  RegionLayout L;
+  L.off_count = kSigBytes;
+  L.count_stride = align256((size_t)world * E * sizeof(int32_t));
+  L.off_fansrc = L.off_count + 2 * L.count_stride;
+  L.fansrc_stride = align256((size_t)max_rows * sizeof(int32_t));
+  L.off_act = L.off_fansrc + 2 * L.fansrc_stride;
+  L.act_stride = align256((size_t)max_rows * (size_t)tb);
+  L.off_actout = L.off_act + 2 * L.act_stride;
+  L.total = L.off_actout + (with_act_out ? L.act_stride : 0);
+  return L;
+}
+
+}  // namespace
+
+struct fs_ctx {
+  int rank, world, E, K, tb, max_tokens, with_act_out;
+  long long max_rows;
+  int device;
+  int nloc;
+  int layout_grid_max;  // cooperative capacity of the layout kernel
+  int move_grid;        // dispatch persistent grid (equal on all ranks)
+  int sms;
+  int combine_grid_cap; // 0 = occupancy-derived
+  size_t layout_smem;
+  uint32_t epoch;
+  unsigned long long timeout_ns;
+  RegionLayout L;
+  std::vector<char*> peers;
+  int32_t *owner_d, *node_of_d, *perm_d, *seg_d, *chunk_cnt_d;
+  long long* stat_part_d;
+  int* status_d;
+  int* num_rows_d;
+};
+
+namespace {
+
+FsArgs make_args(const fs_ctx* h, int T, int idx64) {
+  FsArgs a;
+  memset(&a, 0, sizeof(a));
+  a.rank = h->rank;
+  a.world = h->world;
+  a.E = h->E;
+  a.K = h->K;
+  a.tb = h->tb;
+  a.T = T;
+  a.idx64 = idx64;
+  a.epoch = h->epoch;
+  a.parity = (int)(h->epoch & 1u);
+  a.max_rows = h->max_rows;
+  a.owner = h->owner_d;
+  a.node_of = h->node_of_d;
+  a.perm = h->perm_d;
+  a.seg_begin = h->seg_d;
+  for (int g = 0; g < h->world; ++g) a.peer[g] = h->peers[g];
+  a.off_count = h->L.off_count;
+  a.off_fansrc = h->L.off_fansrc;
+  a.off_act = h->L.off_act;
+  a.off_actout = h->L.off_actout;
+  a.count_stride = h->L.count_stride;
+  a.fansrc_stride = h->L.fansrc_stride;
+  a.act_stride = h->L.act_stride;
+  a.chunk_cnt = h->chunk_cnt_d;
+  a.stat_part = h->stat_part_d;
+  a.status = h->status_d;
+  a.num_rows = h->num_rows_d;
+  a.timeout_ns = h->timeout_ns;
+  return a;
+}
+
+int check_idx_bytes(int idx_bytes) {
+  if (idx_bytes != 4 && idx_bytes != 8) return fail(FS_EINVAL, "idx_bytes must be 4 or 8");
+  return FS_OK;
+}
+
+bool aligned(const void* p, size_t n) { return (reinterpret_cast<uintptr_t>(p) % n) == 0; }
+
+template <typename Kern>
+int occupancy(Kern kernel, int threads, size_t smem, int* out) {
+  FS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, kernel, threads, smem));
+  return FS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fs_abi_version(void) { return FS_ABI_VERSION; }
+
+const char* fs_last_error(void) { return g_err.c_str(); }
+
+int fs_region_bytes(int world, int num_experts, int token_bytes, long long max_rows, int with_act_out,
+                    size_t* bytes_out) {
+  if (!bytes_out || world < 1 || world > FS_MAX_RANKS || num_experts < 1 || token_bytes <= 0 ||
+      max_rows < 0)
+    return fail(FS_EINVAL, "fs_region_bytes: bad arguments");
+  *bytes_out = region_layout(world, num_experts, token_bytes, max_rows, with_act_out).total;
+  return FS_OK;
+}
+
+int fs_sym_alloc(int device, size_t bytes, void** ptr_out) {
+  if (!ptr_out || bytes == 0) return fail(FS_EINVAL, "fs_sym_alloc: bad arguments");
+  FS_CUDA(cudaSetDevice(device));
+  void* p = nullptr;
+  FS_CUDA(cudaMalloc(&p, bytes));
+  FS_CUDA(cudaMemset(p, 0, bytes));
+  FS_CUDA(cudaDeviceSynchronize());
+  *ptr_out = p;
+  return FS_OK;
+}
+
+int fs_sym_free(int device, void* ptr) {
+  FS_CUDA(cudaSetDevice(device));
+  if (ptr) FS_CUDA(cudaFree(ptr));
+  return FS_OK;
+}
+
+int fs_ipc_handle(int device, void* ptr, uint8_t* handle64_out) {
+  if (!ptr || !handle64_out) return fail(FS_EINVAL, "fs_ipc_handle: bad arguments");
+  FS_CUDA(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(h) == 64, "CUDA IPC handle is 64 bytes");
+  FS_CUDA(cudaIpcGetMemHandle(&h, ptr));
+  memcpy(handle64_out, &h, 64);
+  return FS_OK;
+}
+
+int fs_ipc_open(int device, const uint8_t* handle64, void** ptr_out) {
+  if (!handle64 || !ptr_out) return fail(FS_EINVAL, "fs_ipc_open: bad arguments");
+  FS_CUDA(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  void* p = nullptr;
+  FS_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  *ptr_out = p;
+  return FS_OK;
+}
+
+int fs_ipc_close(int device, void* ptr) {
+  FS_CUDA(cudaSetDevice(device));
+  if (ptr) FS_CUDA(cudaIpcCloseMemHandle(ptr));
+  return FS_OK;
+}
+
+int fs_create(int device, int rank, int world, int num_experts, int topk, int token_bytes, int max_tokens,
+              long long max_rows, int with_act_out, const int32_t* expert_owner,
+              const int32_t* node_of, void* const* peer_regions, int grid_ctas, int timeout_ms,
+              fs_handle_t* out) {
+  if (!out || !expert_owner || !peer_regions) return fail(FS_EINVAL, "fs_create: null argument");
+  *out = nullptr;
+  if (world < 1 || world > FS_MAX_RANKS) return fail(FS_EINVAL, "world must be in [1, 32]");
+  if (rank < 0 || rank >= world) return fail(FS_EINVAL, "rank outside [0, world)");
+  if (num_experts < 1) return fail(FS_EINVAL, "num_experts must be >= 1");
+  if (topk < 1 || topk > 32 || topk > num_experts)
+    return fail(FS_EINVAL, "topk must be in [1, min(32, num_experts)]");
+  if (token_bytes <= 0 || token_bytes % 4)
+    return fail(FS_EINVAL, "token_bytes must be a positive multiple of 4");
+  if (max_tokens < 0) return fail(FS_EINVAL, "max_tokens must be >= 0");
+  // expert table and per-rank segments (experts sorted by (owner, id))
+  std::vector<int32_t> owner(expert_owner, expert_owner + num_experts);
+  std::vector<int32_t> nodes(world);
+  for (int g = 0; g < world; ++g) nodes[g] = node_of ? node_of[g] : g;
+  for (int e = 0; e < num_experts; ++e)
+    if (owner[e] < 0 || owner[e] >= world) return fail(FS_EINVAL, "expert owner outside [0, world)");
+  for (int g = 0; g < world; ++g)
+    if (nodes[g] < 0 || nodes[g] >= world) return fail(FS_EINVAL, "node_of outside [0, world)");
+  std::vector<int32_t> perm(num_experts), seg(world + 1, 0);
+  for (int e = 0; e < num_experts; ++e) seg[owner[e] + 1]++;
+  for (int g = 0; g < world; ++g) seg[g + 1] += seg[g];
+  {
+    std::vector<int32_t> fill(seg.begin(), seg.end() - 1);
+    for (int e = 0; e < num_experts; ++e) perm[fill[owner[e]]++] = e;
+  }
+  int max_local = 0;
+  for (int g = 0; g < world; ++g) max_local = std::max(max_local, seg[g + 1] - seg[g]);
+  if (max_rows <= 0) max_rows = (long long)world * max_tokens * std::min(topk, std::max(1, max_local));
+  if (max_rows < 1) max_rows = 1;
+  if (max_rows > 0x7fffffffLL) return fail(FS_EINVAL, "max_rows exceeds int32 row indices");
+  for (int g = 0; g < world; ++g)
+    if (!peer_regions[g]) return fail(FS_EINVAL, "peer region pointer is null");
+
+  FS_CUDA(cudaSetDevice(device));
+  fs_ctx* h = new fs_ctx();
+  h->device = device;
+  h->rank = rank;
+  h->world = world;
+  h->E = num_experts;
+  h->K = topk;
+  h->tb = token_bytes;
+  h->max_tokens = max_tokens;
+  h->max_rows = max_rows;
+  h->with_act_out = with_act_out ? 1 : 0;
+  h->nloc = seg[rank + 1] - seg[rank];
+  h->epoch = 0;
+  h->timeout_ns = (unsigned long long)(timeout_ms > 0 ? timeout_ms : 10000) * 1000000ull;
+  h->L = region_layout(world, num_experts, token_bytes, max_rows, h->with_act_out);
+  h->peers.assign((char* const*)peer_regions, (char* const*)peer_regions + world);
+  h->layout_smem = layout_smem_bytes(num_experts);
+  auto cleanup = [&](int rc) {
+    fs_destroy(h);
+    return rc;
+  };
+  cudaError_t e;
+  int sms = 0;
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+  if (e != cudaSuccess) return cleanup(fail(FS_ECUDA, cudaGetErrorString(e)));
+
+  if (h->layout_smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)h->layout_smem);
+    if (e != cudaSuccess) return cleanup(fail(FS_ECUDA, cudaGetErrorString(e)));
+  }
+  int occ_l = 0;
+  int rc = occupancy(layout_kernel, kLayoutThreads, h->layout_smem, &occ_l);
+  if (rc) return cleanup(rc);
+  if (occ_l < 1) return cleanup(fail(FS_EINVAL, "layout kernel cannot be resident (too many experts)"));
+  const int max_chunks = std::max(1, (max_tokens + kLayoutThreads - 1) / kLayoutThreads);
+  h->layout_grid_max = std::min(max_chunks, occ_l * sms);
+
+  // Dispatch grid: part of the cross-rank arrival count, so it must be equal
+  // on every rank (same GPU model -> same occupancy -> same grid).
+  int occ_d = 0;
+  if ((rc = occupancy(dispatch_kernel<int4>, kMoveThreads, 0, &occ_d))) return cleanup(rc);
+  int o = 0;
+  if ((rc = occupancy(dispatch_kernel<int>, kMoveThreads, 0, &o))) return cleanup(rc);
+  occ_d = std::max(1, std::min(std::min(occ_d, o), kMaxCtasPerSm));
+  h->move_grid = grid_ctas > 0 ? std::min(grid_ctas, occ_d * sms) : occ_d * sms;
+  h->sms = sms;
+  h->combine_grid_cap = grid_ctas > 0 ? grid_ctas : 0;
+
+  auto dalloc = [&](void** p, size_t n) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(n, 16)); };
+  if ((e = dalloc((void**)&h->owner_d, num_experts * 4)) != cudaSuccess ||
+      (e = dalloc((void**)&h->node_of_d, world * 4)) != cudaSuccess ||
+      (e = dalloc((void**)&h->perm_d, num_experts * 4)) != cudaSuccess ||
+      (e = dalloc((void**)&h->seg_d, (world + 1) * 4)) != cudaSuccess ||
+      (e = dalloc((void**)&h->chunk_cnt_d, (size_t)max_chunks * num_experts * 4)) != cudaSuccess ||
+      (e = dalloc((void**)&h->stat_part_d, (size_t)h->layout_grid_max * 8 * 8)) != cudaSuccess ||
+      (e = dalloc((void**)&h->status_d, 4)) != cudaSuccess ||
+      (e = dalloc((void**)&h->num_rows_d, 4)) != cudaSuccess)
+    return cleanup(fail(FS_ECUDA, std::string("fs_create alloc: ") + cudaGetErrorString(e)));
+  if ((e = cudaMemcpy(h->owner_d, owner.data(), num_experts * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(h->node_of_d, nodes.data(), world * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(h->perm_d, perm.data(), num_experts * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(h->seg_d, seg.data(), (world + 1) * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemset(h->status_d, 0, 4)) != cudaSuccess ||
+      (e = cudaMemset(h->num_rows_d, 0, 4)) != cudaSuccess ||
+      (e = cudaDeviceSynchronize()) != cudaSuccess)
+    return cleanup(fail(FS_ECUDA, std::string("fs_create init: ") + cudaGetErrorString(e)));
+  *out = h;
+  return FS_OK;
+}
+
+int fs_destroy(fs_handle_t h) {
+  if (!h) return FS_OK;
+  cudaSetDevice(h->device);
+  cudaFree(h->owner_d);
+  cudaFree(h->node_of_d);
+  cudaFree(h->perm_d);
+  cudaFree(h->seg_d);
+  cudaFree(h->chunk_cnt_d);
+  cudaFree(h->stat_part_d);
+  cudaFree(h->status_d);
+  cudaFree(h->num_rows_d);
+  delete h;
+  return FS_OK;
+}
+
+int fs_num_local_experts(fs_handle_t h, int* n_out) {
+  if (!h || !n_out) return fail(FS_EINVAL, "null argument");
+  *n_out = h->nloc;
+  return FS_OK;
+}
+
+int fs_grid_ctas(fs_handle_t h, int* n_out) {
+  if (!h || !n_out) return fail(FS_EINVAL, "null argument");
+  *n_out = h->move_grid;
+  return FS_OK;
+}
+
+int fs_buffer_ptr(fs_handle_t h, int which, void** ptr_out) {
+  if (!h || !ptr_out) return fail(FS_EINVAL, "null argument");
+  char* base = h->peers[h->rank];
+  if (which == 0) {
+    *ptr_out = base + h->L.off_act + (size_t)(h->epoch & 1u) * h->L.act_stride;
+  } else if (which == 1) {
+    if (!h->with_act_out) return fail(FS_EINVAL, "handle was created without an act_out buffer");
+    *ptr_out = base + h->L.off_actout;
+  } else {
+    return fail(FS_EINVAL, "which must be 0 (act) or 1 (act_out)");
+  }
+  return FS_OK;
+}
+
+long long fs_max_rows(fs_handle_t h) { return h ? h->max_rows : -1; }
+
+unsigned int fs_epoch(fs_handle_t h) { return h ? h->epoch : 0u; }
+
+int fs_layout(fs_handle_t h, const void* topk_idx, int idx_bytes, int num_tokens, int32_t* row_of,
+              int32_t* expert_counts, int32_t* expert_offsets, uint8_t* first_mask,
+              uint32_t* rank_mask, int64_t* stats, int phase, void* stream) {
+  if (!h) return fail(FS_EINVAL, "null handle");
+  FS_CUDA(cudaSetDevice(h->device));
+  if (int rc = check_idx_bytes(idx_bytes)) return rc;
+  if (num_tokens < 0 || num_tokens > h->max_tokens)
+    return fail(FS_EINVAL, "num_tokens outside [0, max_tokens]");
+  if ((phase & FS_PHASE_ALL) == 0 || (phase & ~FS_PHASE_ALL)) return fail(FS_EINVAL, "bad phase");
+  if (num_tokens > 0 && (!topk_idx || !row_of)) return fail(FS_EINVAL, "null topk_idx / row_of");
+  if (phase & FS_PHASE_LOCAL) h->epoch++;
+  FsArgs a = make_args(h, num_tokens, idx_bytes == 8);
+  const int nchunks = (num_tokens + kLayoutThreads - 1) / kLayoutThreads;
+  const int grid = std::max(1, std::min(nchunks, h->layout_grid_max));
+  long long* st = reinterpret_cast<long long*>(stats);
+  void* args[] = {&a, (void*)&topk_idx, &row_of, &first_mask, &rank_mask,
+                  &st, &expert_counts, &expert_offsets, &phase};
+  FS_CUDA(cudaLaunchCooperativeKernel((const void*)layout_kernel, dim3(grid), dim3(kLayoutThreads), args,
+                                      h->layout_smem, (cudaStream_t)stream));
+  return FS_OK;
+}
+
+int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_bytes, const int32_t* row_of,
+                int num_tokens, int phase, void* stream) {
+  if (!h) return fail(FS_EINVAL, "null handle");
+  FS_CUDA(cudaSetDevice(h->device));
+  if (int rc = check_idx_bytes(idx_bytes)) return rc;
+  if (num_tokens < 0 || num_tokens > h->max_tokens)
+    return fail(FS_EINVAL, "num_tokens outside [0, max_tokens]");
+  if ((phase & FS_PHASE_ALL) == 0 || (phase & ~FS_PHASE_ALL)) return fail(FS_EINVAL, "bad phase");
+  if (num_tokens > 0 && (!x || !topk_idx || !row_of)) return fail(FS_EINVAL, "null input");
+  if (h->epoch == 0) return fail(FS_EINVAL, "fs_dispatch before fs_layout");
+  FsArgs a = make_args(h, num_tokens, idx_bytes == 8);
+  const bool vec16 = (h->tb % 16 == 0) && aligned(x, 16);
+  if (!aligned(x, 4)) return fail(FS_EINVAL, "x must be 4-byte aligned");
+  void* args[] = {&a, (void*)&x, (void*)&topk_idx, (void*)&row_of, &phase};
+  const void* fn = vec16 ? (const void*)dispatch_kernel<int4> : (const void*)dispatch_kernel<int>;
+  // fixed grid: receivers expect epoch * world * move_grid arrival signals
+  FS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(h->move_grid), dim3(kMoveThreads), args, 0,
+                                      (cudaStream_t)stream));
+  return FS_OK;
+}
+
+int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes, const int32_t* row_of, const void* topk_w,
+               int w_bytes, int num_tokens, void* out, int dtype, int src, int acc, int phase,
+               void* stream) {
+  if (!h) return fail(FS_EINVAL, "null handle");
+  FS_CUDA(cudaSetDevice(h->device));
+  if (int rc = check_idx_bytes(idx_bytes)) return rc;
+  if (w_bytes != 4 && w_bytes != 8) return fail(FS_EINVAL, "w_bytes must be 4 or 8");
+  if (num_tokens < 0 || num_tokens > h->max_tokens)
+    return fail(FS_EINVAL, "num_tokens outside [0, max_tokens]");
+  if ((phase & FS_PHASE_ALL) == 0 || (phase & ~FS_PHASE_ALL)) return fail(FS_EINVAL, "bad phase");
+  if (dtype != FS_DTYPE_F32 && dtype != FS_DTYPE_BF16) return fail(FS_EINVAL, "dtype must be f32 or bf16");
+  if (src != FS_SRC_ACT && src != FS_SRC_ACT_OUT) return fail(FS_EINVAL, "src must be act or act_out");
+  if (src == FS_SRC_ACT_OUT && !h->with_act_out)
+    return fail(FS_EINVAL, "combine from act_out on a handle without act_out");
+  if (acc != FS_ACC_F32 && acc != FS_ACC_F64) return fail(FS_EINVAL, "acc must be f32 or f64");
+  if (num_tokens > 0 && (!topk_idx || !row_of || !topk_w || !out)) return fail(FS_EINVAL, "null input");
+  if (h->epoch == 0) return fail(FS_EINVAL, "fs_combine before fs_layout");
+  FsArgs a = make_args(h, num_tokens, idx_bytes == 8);
+  if (!aligned(out, 4)) return fail(FS_EINVAL, "out must be 4-byte aligned");
+  const bool vec16 = (h->tb % 16 == 0) && aligned(out, 16);
+  int w64 = w_bytes == 8;
+  void* args[] = {&a, (void*)&topk_idx, (void*)&row_of, (void*)&topk_w, &w64, &out, &src, &phase};
+  const void* fn;
+  const bool bf = dtype == FS_DTYPE_BF16, f64 = acc == FS_ACC_F64;
+  if (vec16) {
+    fn = bf ? (f64 ? (const void*)combine_kernel<int4, true, true> : (const void*)combine_kernel<int4, true, false>)
+            : (f64 ? (const void*)combine_kernel<int4, false, true> : (const void*)combine_kernel<int4, false, false>);
+  } else {
+    fn = bf ? (f64 ? (const void*)combine_kernel<int, true, true> : (const void*)combine_kernel<int, true, false>)
+            : (f64 ? (const void*)combine_kernel<int, false, true> : (const void*)combine_kernel<int, false, false>);
+  }
+  int occ = 0;
+  if (int rc = occupancy(fn, kMoveThreads, 0, &occ)) return rc;
+  occ = std::max(1, std::min(occ, kMaxCtasPerSm));
+  int grid = occ * h->sms;
+  if (h->combine_grid_cap > 0) grid = std::min(grid, h->combine_grid_cap);
+  FS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kMoveThreads), args, 0, (cudaStream_t)stream));
+  return FS_OK;
+}
+
+int fs_check(fs_handle_t h, void* stream) {
+  if (!h) return fail(FS_EINVAL, "null handle");
+  FS_CUDA(cudaSetDevice(h->device));
+  FS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  int status = 0;
+  FS_CUDA(cudaMemcpy(&status, h->status_d, 4, cudaMemcpyDeviceToHost));
+  FS_CUDA(cudaMemset(h->status_d, 0, 4));
+  if (status == FS_ETIMEOUT) return fail(FS_ETIMEOUT, "a peer flag wait timed out");
+  if (status == FS_ERANGE) return fail(FS_ERANGE, "routing out of range (expert id or row capacity)");
+  if (status == FS_EINVAL) return fail(FS_EINVAL, "a token routes to the same expert twice");
+  if (status != FS_OK) return fail(status, "device reported an error");
+  return FS_OK;
+}
+
+int fs_probe_copy(int device, void* dst, const void* src, size_t bytes, int ctas, void* stream) {
+  FS_CUDA(cudaSetDevice(device));
+  if (!dst || !src || bytes % 16 || !aligned(dst, 16) || !aligned(src, 16))
+    return fail(FS_EINVAL, "fs_probe_copy: 16-byte aligned buffers and size required");
+  if (ctas <= 0) return fail(FS_EINVAL, "fs_probe_copy: ctas must be > 0");
+  probe_copy_kernel<<<ctas, kMoveThreads, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<int4*>(dst), reinterpret_cast<const int4*>(src), bytes / 16);
+  FS_CUDA(cudaGetLastError());
+  return FS_OK;
+}
+
+}  // extern "C"

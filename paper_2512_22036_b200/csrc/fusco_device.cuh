@@ -1,0 +1,165 @@
+// fusco_device.cuh — device-side primitives for the NVLink shuffle kernels.
+//
+// Memory-ordering protocol over NVLink/NVSwitch (replaces the reference's
+// ring-buffer + expected-byte counters, engine.py:637-694, 979-1031):
+//   writer: payload stores (weak st.global to peer addresses)
+//           -> fence.sc.sys by every writing thread -> bar.sync
+//           -> one thread: st.release.sys / red.release.sys on the peer flag
+//   reader: one thread per flag spins ld.acquire.sys until the epoch value
+//           -> bar.sync -> payload loads.
+// Flags never reset: they carry the monotonically increasing epoch (or an
+// epoch-scaled arrival count), so consecutive iterations need no barrier.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/fusco.h"
+
+namespace fusco {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+// Offsets inside the 4 KiB signal block at the start of every region.
+constexpr size_t kSigBytes = 4096;
+constexpr size_t kOffCountFlag = 0;    // u32[FS_MAX_RANKS]: layout counts published
+constexpr size_t kOffReadyFlag = 256;  // u32[FS_MAX_RANKS]: expert outputs ready
+constexpr size_t kOffArrive = 512;     // u64: dispatch CTAs that finished pushing here
+
+struct FsArgs {
+  int rank, world, E, K, tb, T;
+  int idx64;      // topk_idx element size 8 (else 4)
+  int parity;     // epoch & 1: which act / count / fan_src copy
+  uint32_t epoch;
+  long long max_rows;
+  const int32_t* owner;      // [E] expert -> rank
+  const int32_t* node_of;    // [P] rank -> node (first_mask statistics)
+  const int32_t* perm;       // [E] experts sorted by (owner, id)
+  const int32_t* seg_begin;  // [P+1] segment of rank g in perm
+  char* peer[FS_MAX_RANKS];  // every rank's region, mapped here
+  size_t off_count, off_fansrc, off_act, off_actout;
+  size_t count_stride, fansrc_stride, act_stride;  // bytes per parity copy
+  int32_t* chunk_cnt;        // [chunks][E] scratch (per handle)
+  long long* stat_part;      // [layout grid][8] scratch
+  int* status;               // first error code, FS_OK when clean
+  int* num_rows;             // rows of the own activation buffer this epoch
+  unsigned long long timeout_ns;
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void record_error(int* status, int code) {
+  atomicCAS(status, FS_OK, code);
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_relaxed_sys_s32(const int32_t* p) {
+  int v;
+  asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_sys_add_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Spin until *p >= target (wrap-safe for u32 epochs); false on timeout.
+__device__ __forceinline__ bool wait_u32_geq(const uint32_t* p, uint32_t target, const FsArgs& a) {
+  const unsigned long long t0 = globaltimer();
+  while ((int32_t)(ld_acquire_sys_u32(p) - target) < 0) {
+    if (globaltimer() - t0 > a.timeout_ns) {
+      record_error(a.status, FS_ETIMEOUT);
+      return false;
+    }
+  }
+  return true;
+}
+__device__ __forceinline__ bool wait_u64_geq(const unsigned long long* p, unsigned long long target,
+                                             const FsArgs& a) {
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire_sys_u64(p) < target) {
+    if (globaltimer() - t0 > a.timeout_ns) {
+      record_error(a.status, FS_ETIMEOUT);
+      return false;
+    }
+  }
+  return true;
+}
+
+// ---- 16-byte / 4-byte vector moves ----------------------------------------
+// Read-only inputs (x, peers' finished act/act_out): non-coherent path, no L1
+// allocation (streaming).  Data written by peers inside the same kernel
+// (fan-out sources): .cg (L2, coherent).  Stores: plain weak st.global; the
+// release fence publishes them.
+__device__ __forceinline__ int4 ld_nc(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int ld_nc(const int* p) {
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int4 ld_cg(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int ld_cg(const int* p) {
+  int r;
+  asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_na(int4* p, const int4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void st_na(int* p, const int& v) {
+  asm volatile("st.global.L1::no_allocate.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <typename V>
+__device__ __forceinline__ uint32_t word(const V& v, int j) {
+  return reinterpret_cast<const uint32_t*>(&v)[j];
+}
+template <typename V>
+__device__ __forceinline__ void set_word(V& v, int j, uint32_t x) {
+  reinterpret_cast<uint32_t*>(&v)[j] = x;
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int n = __shfl_up_sync(kFull, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+
+__device__ __forceinline__ long long load_idx(const void* idx, size_t pos, int idx64) {
+  return idx64 ? reinterpret_cast<const long long*>(idx)[pos]
+               : (long long)reinterpret_cast<const int32_t*>(idx)[pos];
+}
+
+}  // namespace fusco

@@ -1,0 +1,535 @@
+// fusco_kernels.cuh — the three hot-path kernels of the shuffle.
+//
+//   layout_kernel    on-device planner: per-(rank, expert) counts, offsets,
+//                    row_of[t,k], first_mask, dedup statistics
+//                    (reference planner.py:126-196, routing.py:86-98)
+//   dispatch_kernel  push: token rows -> owners' expert-major rows over NVLink,
+//                    one crossing per (token, rank), receiver-side fan-out
+//                    (reference engine.py:266-276 dispatch, 799-851)
+//   combine_kernel   pull + k-ascending weighted reduction back to token order
+//                    (reference engine.py:266-276 combine, 313-338, 967-1049)
+//
+// All three are persistent cooperative launches; their cross-rank waits are
+// split into an explicit REMOTE phase so that P ranks can be emulated on one
+// GPU by launching LOCAL for every rank, then REMOTE for every rank.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "fusco_device.cuh"
+
+namespace fusco {
+namespace cg = cooperative_groups;
+
+constexpr int kLayoutThreads = 256;  // one token per thread per chunk
+constexpr int kLayoutWarps = kLayoutThreads / 32;
+constexpr int kMoveThreads = 256;    // dispatch / combine CTA size
+
+// Shared memory of the layout kernel: LOCAL needs two [8][E] bit tables,
+// REMOTE three [E] int tables.
+__host__ __device__ inline size_t layout_smem_bytes(int E) {
+  const size_t a = 2ull * kLayoutWarps * E * sizeof(uint32_t);
+  const size_t b = 3ull * E * sizeof(int32_t);
+  return a > b ? a : b;
+}
+
+// ===========================================================================
+// Layout planner
+//
+// Row order on rank g (Appendix A of SURVEY.md, planner.py:147-151):
+//   rows sorted by (expert asc, source rank asc, local token index asc)
+//   row_of[i,k] = base_g(e) + Σ_{s'<s} cnt[s'][e] + chunk_off[c][e]
+//                 + (position of token i among chunk c's tokens routed to e)
+// The in-chunk position is computed without atomics on positions: each warp
+// ORs a lane bit into a per-(warp, expert) word; a token's rank among the
+// earlier tokens of its warp is popc(word & lanemask_lt), plus the sum of the
+// popcounts of the earlier warps.  Deterministic, hence bit-exact.
+// ===========================================================================
+__global__ void __launch_bounds__(kLayoutThreads)
+    layout_kernel(FsArgs a, const void* __restrict__ idx, int32_t* __restrict__ row_of,
+                  uint8_t* __restrict__ first_mask, uint32_t* __restrict__ rank_mask,
+                  long long* __restrict__ stats, int32_t* __restrict__ expert_counts,
+                  int32_t* __restrict__ expert_offsets, int phase) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  __shared__ long long red[kLayoutWarps][4];
+  __shared__ int rows_total;
+  cg::grid_group grid = cg::this_grid();
+  const int E = a.E, K = a.K, T = a.T, P = a.world, s = a.rank;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nchunks = (T + kLayoutThreads - 1) / kLayoutThreads;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+
+  if (phase & FS_PHASE_LOCAL) {
+    uint32_t* bits = sm;                       // [8][E]
+    uint32_t* wbase = sm + kLayoutWarps * E;   // [8][E]
+    long long st_dedup = 0, st_naive = 0, st_local = 0, st_node = 0;
+    const int my_node = a.node_of[s];
+    for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
+      for (int j = tid; j < kLayoutWarps * E; j += kLayoutThreads) bits[j] = 0u;
+      __syncthreads();
+      const int i = c * kLayoutThreads + tid;
+      if (i < T) {
+        uint32_t seen_node = 0u, seen_rank = 0u;
+        for (int k = 0; k < K; ++k) {
+          long long e = load_idx(idx, (size_t)i * K + k, a.idx64);
+          if (e < 0 || e >= E) {
+            record_error(a.status, FS_ERANGE);
+            e = 0;
+          }
+          const int g = a.owner[e];
+          const int n = a.node_of[g];
+          const bool first = !((seen_node >> n) & 1u);
+          seen_node |= 1u << n;
+          seen_rank |= 1u << g;
+          if (first_mask) first_mask[(size_t)i * K + k] = first ? 1 : 0;
+          st_naive += (g != s);
+          st_local += (g == s);
+          st_node += (first && n != my_node);
+          const uint32_t old = atomicOr(&bits[warp * E + e], 1u << lane);
+          if (old & (1u << lane)) record_error(a.status, FS_EINVAL);  // duplicate expert in a row
+        }
+        if (rank_mask) rank_mask[i] = seen_rank;
+        st_dedup += __popc(seen_rank & ~(1u << s));
+      }
+      __syncthreads();
+      for (int e = tid; e < E; e += kLayoutThreads) {
+        uint32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < kLayoutWarps; ++w) {
+          wbase[w * E + e] = run;
+          run += __popc(bits[w * E + e]);
+        }
+        a.chunk_cnt[(size_t)c * E + e] = (int32_t)run;
+      }
+      __syncthreads();
+      if (i < T) {
+        for (int k = 0; k < K; ++k) {
+          long long e = load_idx(idx, (size_t)i * K + k, a.idx64);
+          if (e < 0 || e >= E) e = 0;
+          row_of[(size_t)i * K + k] =
+              (int32_t)(wbase[warp * E + e] + __popc(bits[warp * E + e] & lt_mask));
+        }
+      }
+      __syncthreads();
+    }
+    // block-reduce the statistics into the per-CTA partial slot
+    long long v[4] = {st_dedup, st_naive, st_local, st_node};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_xor_sync(kFull, v[j], o);
+      if (lane == 0) red[warp][j] = v[j];
+    }
+    __syncthreads();
+    if (tid < 4) {
+      long long acc = 0;
+      for (int w = 0; w < kLayoutWarps; ++w) acc += red[w][tid];
+      a.stat_part[blockIdx.x * 8 + tid] = acc;
+    }
+    grid.sync();
+
+    // Exclusive scan of every expert's chunk counts (one warp per expert),
+    // then publish this rank's per-expert totals into every peer's count
+    // matrix row [s] (the 8 KB "all-gather" of the P x E count matrix).
+    const int gw = blockIdx.x * kLayoutWarps + warp, nw = gridDim.x * kLayoutWarps;
+    for (int e = gw; e < E; e += nw) {
+      int run = 0;
+      for (int cb = 0; cb < nchunks; cb += 32) {
+        const int c = cb + lane;
+        const int val = c < nchunks ? a.chunk_cnt[(size_t)c * E + e] : 0;
+        const int incl = warp_incl_scan(val, lane);
+        if (c < nchunks) a.chunk_cnt[(size_t)c * E + e] = run + incl - val;
+        run += __shfl_sync(kFull, incl, 31);
+      }
+      for (int g = lane; g < P; g += 32) {
+        int32_t* dst = reinterpret_cast<int32_t*>(a.peer[g] + a.off_count +
+                                                  (size_t)a.parity * a.count_stride);
+        dst[(size_t)s * E + e] = run;
+      }
+    }
+    __threadfence_system();
+    grid.sync();
+    if (blockIdx.x == 0) {
+      if (tid < P)
+        st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[tid] + kOffCountFlag) + s, a.epoch);
+      if (stats && tid < 4) {
+        long long acc = 0;
+        for (int b = 0; b < (int)gridDim.x; ++b) acc += a.stat_part[b * 8 + tid];
+        const int slot[4] = {FS_STAT_DEDUP_SEND, FS_STAT_NAIVE_SEND, FS_STAT_LOCAL_ROWS,
+                             FS_STAT_NODE_DEDUP};
+        stats[slot[tid]] = acc;
+      }
+      if (stats && tid >= 5 && tid < FS_NSTATS) stats[tid] = 0;
+    }
+  }
+
+  if (phase & FS_PHASE_REMOTE) {
+    if (tid < P)
+      wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffCountFlag) + tid, a.epoch, a);
+    __syncthreads();
+    int32_t* tot = reinterpret_cast<int32_t*>(sm);
+    int32_t* base = tot + E;
+    int32_t* before = base + E;
+    const int32_t* cnt =
+        reinterpret_cast<const int32_t*>(a.peer[s] + a.off_count + (size_t)a.parity * a.count_stride);
+    for (int e = tid; e < E; e += kLayoutThreads) {
+      int t = 0, b = 0;
+      for (int q = 0; q < P; ++q) {
+        const int val = ld_relaxed_sys_s32(cnt + (size_t)q * E + e);
+        t += val;
+        if (q < s) b += val;
+      }
+      tot[e] = t;
+      before[e] = b;
+    }
+    __syncthreads();
+    // base_g(e): exclusive scan of totals over rank g's experts (one warp per rank)
+    for (int g = warp; g < P; g += kLayoutWarps) {
+      int run = 0;
+      const int jb = a.seg_begin[g], je = a.seg_begin[g + 1];
+      for (int j0 = jb; j0 < je; j0 += 32) {
+        const int j = j0 + lane;
+        const int e = j < je ? a.perm[j] : -1;
+        const int val = e >= 0 ? tot[e] : 0;
+        const int incl = warp_incl_scan(val, lane);
+        if (e >= 0) base[e] = run + incl - val;
+        run += __shfl_sync(kFull, incl, 31);
+      }
+      if (g == s && lane == 0) rows_total = run;
+    }
+    __syncthreads();
+    for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
+      const int i = c * kLayoutThreads + tid;
+      if (i < T) {
+        for (int k = 0; k < K; ++k) {
+          long long e = load_idx(idx, (size_t)i * K + k, a.idx64);
+          if (e < 0 || e >= E) e = 0;
+          const size_t pos = (size_t)i * K + k;
+          const long long r =
+              (long long)row_of[pos] + base[e] + before[e] + a.chunk_cnt[(size_t)c * E + e];
+          if (r >= a.max_rows) record_error(a.status, FS_ERANGE);
+          row_of[pos] = (int32_t)r;
+        }
+      }
+    }
+    if (blockIdx.x == 0) {
+      const int jb = a.seg_begin[s], je = a.seg_begin[s + 1];
+      for (int j = jb + tid; j < je; j += kLayoutThreads) {
+        const int e = a.perm[j];
+        if (expert_counts) expert_counts[j - jb] = tot[e];
+        if (expert_offsets) expert_offsets[j - jb] = base[e];
+      }
+      if (tid == 0) {
+        if (expert_offsets) expert_offsets[je - jb] = rows_total;
+        *a.num_rows = rows_total;
+        if (stats) stats[FS_STAT_ROWS] = rows_total;
+        if (rows_total > a.max_rows) record_error(a.status, FS_ERANGE);
+      }
+    }
+  }
+}
+
+// ===========================================================================
+// Dispatch
+//
+// Work unit = (token, slice of SLICE = 32 lanes x U vector words).  Lane k<K
+// of the warp holds (owner g_k, row r_k) of the token's k-th expert.  Per
+// destination rank only the first k crosses NVLink (the per-rank dedup of
+// routing.py:94-97 / planner.py:231 with one GPU per "node"); for the own
+// rank every k is written directly from registers.  The sender records, for
+// each destination row, the row holding its bytes (fan_src): itself, or the
+// primary row of the same token on that rank.  After every source's CTAs
+// have signalled arrival, the receiver copies primary -> duplicate rows in
+// its own HBM.  The activation buffer is double-buffered by epoch parity so
+// that a fast rank's next dispatch cannot overwrite rows a slow rank is
+// still pulling in combine.
+// ===========================================================================
+template <typename V>
+struct MoveCfg {
+  static constexpr int U = sizeof(V) == 16 ? 4 : 8;  // words per lane per unit
+  static constexpr int kSliceWords = 32 * U;
+};
+
+template <typename V>
+__device__ __forceinline__ void warp_copy_row_cg(V* __restrict__ dst, const V* __restrict__ src, int nv,
+                                                 int lane) {
+  constexpr int U = MoveCfg<V>::U;
+  for (int w0 = 0; w0 < nv; w0 += 32 * U) {
+    V v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int w = w0 + j * 32 + lane;
+      if (w < nv) v[j] = ld_cg(src + w);
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int w = w0 + j * 32 + lane;
+      if (w < nv) st_na(dst + w, v[j]);
+    }
+  }
+}
+
+template <typename V>
+__global__ void __launch_bounds__(kMoveThreads)
+    dispatch_kernel(FsArgs a, const V* __restrict__ x, const void* __restrict__ idx,
+                    const int32_t* __restrict__ row_of, int phase) {
+  constexpr int U = MoveCfg<V>::U;
+  constexpr int SW = MoveCfg<V>::kSliceWords;
+  const int K = a.K, T = a.T, P = a.world, s = a.rank;
+  const int nv = a.tb / (int)sizeof(V);
+  const int S = (nv + SW - 1) / SW;
+  const int lane = threadIdx.x & 31;
+  const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  const size_t act_off = a.off_act + (size_t)a.parity * a.act_stride;
+  const size_t fan_off = a.off_fansrc + (size_t)a.parity * a.fansrc_stride;
+
+  if (phase & FS_PHASE_LOCAL) {
+    const long long units = (long long)T * S;
+    for (long long u = gw; u < units; u += nw) {
+      const int i = (int)(u / S);
+      const int sl = (int)(u - (long long)i * S);
+      int g = -1 - lane, r = -1;  // lanes >= K get unique negative keys
+      if (lane < K) {
+        long long e = load_idx(idx, (size_t)i * K + lane, a.idx64);
+        if (e < 0 || e >= a.E) e = 0;
+        g = a.owner[e];
+        r = row_of[(size_t)i * K + lane];
+        if (r < 0 || r >= a.max_rows) r = -1;
+      }
+      const uint32_t same = __match_any_sync(kFull, g);
+      const int first_lane = __ffs(same) - 1;
+      const int r_first = __shfl_sync(kFull, r, first_lane);
+      const bool direct = lane < K && r >= 0 && (first_lane == lane || g == s);
+      const uint32_t dmask = __ballot_sync(kFull, direct);
+      if (sl == 0 && lane < K && r >= 0) {
+        int32_t* fs = reinterpret_cast<int32_t*>(a.peer[g] + fan_off);
+        fs[r] = direct ? r : r_first;
+      }
+      const int w0 = sl * SW;
+      const V* src = x + (size_t)i * nv + w0;
+      const int rem = nv - w0;
+      V v[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int w = j * 32 + lane;
+        if (w < rem) v[j] = ld_nc(src + w);
+      }
+      // Rotate the destination order by token so concurrent warps of this
+      // rank spread their first stores over different peers.
+      uint32_t m = dmask;
+      const int rot = (i + s) % K;
+      m = (m >> rot) | (rot ? (m << (32 - rot)) : 0u);
+      while (m) {
+        const int d0 = __ffs(m) - 1;
+        m &= m - 1;
+        const int d = (d0 + rot) & 31;
+        const int gd = __shfl_sync(kFull, g, d);
+        const int rd = __shfl_sync(kFull, r, d);
+        V* dst = reinterpret_cast<V*>(a.peer[gd] + act_off) + (size_t)rd * nv + w0;
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const int w = j * 32 + lane;
+          if (w < rem) st_na(dst + w, v[j]);
+        }
+      }
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x < P)
+      red_release_sys_add_u64(
+          reinterpret_cast<unsigned long long*>(a.peer[threadIdx.x] + kOffArrive), 1ull);
+  }
+
+  if ((phase & FS_PHASE_REMOTE) && P > 1) {
+    if (threadIdx.x == 0)
+      wait_u64_geq(reinterpret_cast<const unsigned long long*>(a.peer[s] + kOffArrive),
+                   (unsigned long long)a.epoch * (unsigned long long)P * gridDim.x, a);
+    __syncthreads();
+    const int rows = *reinterpret_cast<volatile int*>(a.num_rows);
+    const int32_t* fs = reinterpret_cast<const int32_t*>(a.peer[s] + fan_off);
+    V* act = reinterpret_cast<V*>(a.peer[s] + act_off);
+    for (int r0 = gw * 32; r0 < rows; r0 += nw * 32) {
+      const int r = r0 + lane;
+      const int f = r < rows ? ld_cg(fs + r) : r;
+      uint32_t need = __ballot_sync(kFull, r < rows && f != r && f >= 0 && f < rows);
+      while (need) {
+        const int d = __ffs(need) - 1;
+        need &= need - 1;
+        const int ff = __shfl_sync(kFull, f, d);
+        warp_copy_row_cg(act + (size_t)(r0 + d) * nv, act + (size_t)ff * nv, nv, lane);
+      }
+    }
+  }
+}
+
+// ===========================================================================
+// Combine
+//
+// out[i] = Σ_{k=0..K-1} w[i,k] · src_{owner(e_ik)}[row_of[i,k]]  (k ascending)
+// pulled straight from the owners' rows; no staging buffer, no second pass.
+// ACC64 reproduces engine.py:322-331 bit for bit (f64 multiply, then f64 add,
+// k ascending, one final rounding); otherwise fp32 FMA.
+// ===========================================================================
+template <typename V, bool BF16>
+struct Elem {
+  static constexpr int kWords = sizeof(V) / 4;
+  static constexpr int kPerWord = BF16 ? 2 : 1;
+  static constexpr int N = kWords * kPerWord;
+  __device__ __forceinline__ static float get(const V& v, int j) {
+    const uint32_t w = word(v, j / kPerWord);
+    if constexpr (BF16) return __uint_as_float((j & 1) ? (w & 0xffff0000u) : (w << 16));
+    else return __uint_as_float(w);
+  }
+};
+
+template <typename Acc>
+__device__ __forceinline__ Acc fma_acc(Acc w, float y, Acc acc);
+template <>
+__device__ __forceinline__ float fma_acc<float>(float w, float y, float acc) {
+  return __fmaf_rn(w, y, acc);
+}
+template <>
+__device__ __forceinline__ double fma_acc<double>(double w, float y, double acc) {
+  return __dadd_rn(acc, __dmul_rn(w, (double)y));  // no contraction: matches numpy
+}
+
+__device__ __forceinline__ uint32_t pack_out(float lo, float hi) {
+  const __nv_bfloat16 a = __float2bfloat16_rn(lo), b = __float2bfloat16_rn(hi);
+  return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
+}
+__device__ __forceinline__ uint32_t pack_out(double lo, double hi) {
+  const __nv_bfloat16 a = __double2bfloat16(lo), b = __double2bfloat16(hi);
+  return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
+}
+__device__ __forceinline__ uint32_t f32_bits(float v) { return __float_as_uint(v); }
+__device__ __forceinline__ uint32_t f32_bits(double v) { return __float_as_uint(__double2float_rn(v)); }
+
+template <typename V, bool BF16, bool ACC64>
+__global__ void __launch_bounds__(kMoveThreads)
+    combine_kernel(FsArgs a, const void* __restrict__ idx, const int32_t* __restrict__ row_of,
+                   const void* __restrict__ topk_w, int w64, V* __restrict__ out, int src_sel,
+                   int phase) {
+  using Acc = typename std::conditional<ACC64, double, float>::type;
+  using EL = Elem<V, BF16>;
+  constexpr int U = sizeof(V) == 16 ? 2 : 4;  // words per lane per unit
+  constexpr int SW = 32 * U;
+  constexpr int KG = 4;                       // experts whose loads are in flight together
+  const int K = a.K, T = a.T, P = a.world, s = a.rank;
+  const int nv = a.tb / (int)sizeof(V);
+  const int S = (nv + SW - 1) / SW;
+  const int lane = threadIdx.x & 31;
+  const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  const size_t src_off =
+      src_sel == FS_SRC_ACT_OUT ? a.off_actout : a.off_act + (size_t)a.parity * a.act_stride;
+
+  if (phase & FS_PHASE_LOCAL) {
+    if (blockIdx.x == 0 && threadIdx.x < P) {
+      __threadfence_system();
+      st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[threadIdx.x] + kOffReadyFlag) + s,
+                         a.epoch);
+    }
+  }
+  if (phase & FS_PHASE_REMOTE) {
+    if (threadIdx.x < P)
+      wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffReadyFlag) + threadIdx.x,
+                   a.epoch, a);
+    __syncthreads();
+    const long long units = (long long)T * S;
+    for (long long u = gw; u < units; u += nw) {
+      const int i = (int)(u / S);
+      const int sl = (int)(u - (long long)i * S);
+      int g = 0, r = 0;
+      Acc wk = (Acc)0;
+      if (lane < K) {
+        const size_t pos = (size_t)i * K + lane;
+        long long e = load_idx(idx, pos, a.idx64);
+        if (e < 0 || e >= a.E) e = 0;
+        g = a.owner[e];
+        r = row_of[pos];
+        if (r < 0 || r >= a.max_rows) r = 0;
+        if (w64) wk = (Acc)reinterpret_cast<const double*>(topk_w)[pos];
+        else wk = (Acc)reinterpret_cast<const float*>(topk_w)[pos];
+      }
+      const int w0 = sl * SW;
+      const int rem = nv - w0;
+      Acc acc[U][EL::N];
+#pragma unroll
+      for (int j = 0; j < U; ++j)
+#pragma unroll
+        for (int q = 0; q < EL::N; ++q) acc[j][q] = (Acc)0;
+      for (int k0 = 0; k0 < K; k0 += KG) {
+        V v[KG][U];
+        Acc wg[KG];
+#pragma unroll
+        for (int kk = 0; kk < KG; ++kk) {
+          const int k = k0 + kk;
+          const int gk = __shfl_sync(kFull, g, k & 31);
+          const int rk = __shfl_sync(kFull, r, k & 31);
+          wg[kk] = __shfl_sync(kFull, wk, k & 31);
+          if (k < K) {
+            const V* src = reinterpret_cast<const V*>(a.peer[gk] + src_off) + (size_t)rk * nv + w0;
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+              const int w = j * 32 + lane;
+              if (w < rem) v[kk][j] = ld_nc(src + w);
+            }
+          }
+        }
+#pragma unroll
+        for (int kk = 0; kk < KG; ++kk) {
+          if (k0 + kk < K) {
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+              if (j * 32 + lane < rem) {
+#pragma unroll
+                for (int q = 0; q < EL::N; ++q)
+                  acc[j][q] = fma_acc<Acc>(wg[kk], EL::get(v[kk][j], q), acc[j][q]);
+              }
+            }
+          }
+        }
+      }
+      V* dst = out + (size_t)i * nv + w0;
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int w = j * 32 + lane;
+        if (w < rem) {
+          V o;
+#pragma unroll
+          for (int q = 0; q < EL::kWords; ++q) {
+            if constexpr (BF16) set_word(o, q, pack_out(acc[j][2 * q], acc[j][2 * q + 1]));
+            else set_word(o, q, f32_bits(acc[j][q]));
+          }
+          st_na(dst + w, o);
+        }
+      }
+    }
+  }
+}
+
+// ===========================================================================
+// Copy-bandwidth probe (HBM or NVLink peer), same warp copy loop shape.
+// ===========================================================================
+__global__ void __launch_bounds__(kMoveThreads)
+    probe_copy_kernel(int4* __restrict__ dst, const int4* __restrict__ src, size_t n16) {
+  constexpr int U = 4;
+  const size_t lane = threadIdx.x & 31;
+  const size_t gw = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  const size_t nw = (gridDim.x * (size_t)blockDim.x) >> 5;
+  for (size_t w0 = gw * 32 * U; w0 < n16; w0 += nw * 32 * U) {
+    int4 v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const size_t w = w0 + j * 32 + lane;
+      if (w < n16) v[j] = ld_nc(src + w);
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const size_t w = w0 + j * 32 + lane;
+      if (w < n16) st_na(dst + w, v[j]);
+    }
+  }
+}
+
+}  // namespace fusco

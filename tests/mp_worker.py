@@ -1,0 +1,72 @@
+"""Per-rank worker for the real multi-GPU parity test (launched by torchrun
+from tests/test_gpu_multiproc.py).  Every rank runs the production path
+(EPBuffer: CUDA-IPC symmetric regions, FS_PHASE_ALL kernels synchronising
+over NVLink flags) and checks its own slice against the oracle."""
+
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+from oracle import shuffle_oracle as O  # noqa: E402
+from paper_2512_22036_b200 import EPBuffer, box, gen_realworld, round_robin_placement  # noqa: E402
+
+
+def main() -> int:
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    P, rank = dist.get_world_size(), dist.get_rank()
+    E, K, H, T_l = int(os.environ.get("MP_E", 64)), int(os.environ.get("MP_K", 8)), 2048, 256
+    topo = box(P)
+    pl = round_robin_placement(E, topo)
+    buf = EPBuffer(num_experts=E, topk=K, hidden=H, dtype="bf16", max_tokens=T_l, timeout_ms=20000)
+    dev = torch.device("cuda", local)
+    failures = 0
+    for it in range(4):
+        a = gen_realworld(P * T_l, K, topo, pl, seed=10 + it, zipf_s=0.4 * it)
+        vals = np.random.default_rng(it).standard_normal((a.num_tokens, H)).astype(np.float32)
+        payload = O.encode(vals, "bf16")
+        ids = np.flatnonzero(a.source == rank)
+        x = torch.as_tensor(payload[ids], device=dev).view(torch.bfloat16).contiguous()
+        idx = torch.as_tensor(a.experts[ids], device=dev)
+        w = torch.as_tensor(a.weights[ids], dtype=torch.float64, device=dev)
+        plan = buf.build_plan(idx)
+        act = buf.dispatch(x, plan)
+        rows = plan.num_rows
+        if it % 2:  # exercise the act_out contract: expert writes into the symmetric buffer
+            buf.expert_out(rows).copy_(act[:rows])
+            out = buf.combine(plan, w, src="act_out", acc="f64")
+        else:
+            out = buf.combine(plan, w, src="act", acc="f64")
+        buf.check()
+        layouts, row_of = O.activation_layouts(a.experts, a.source, pl.owner, P)
+        acts = O.dispatch(payload, layouts)
+        got_act = act[:rows].contiguous().view(torch.uint8).cpu().numpy().reshape(rows, -1)
+        if not np.array_equal(got_act, acts[rank]):
+            print(f"[rank {rank}] iter {it}: activation mismatch", flush=True)
+            failures += 1
+        if not np.array_equal(plan.row_of.cpu().numpy(), row_of[ids]):
+            print(f"[rank {rank}] iter {it}: row_of mismatch", flush=True)
+            failures += 1
+        want = O.combine(acts, row_of, a.experts, a.weights, pl.owner, ids, "bf16")
+        if not np.array_equal(out.view(torch.uint8).cpu().numpy(), want):
+            print(f"[rank {rank}] iter {it}: output mismatch", flush=True)
+            failures += 1
+    t = torch.tensor([failures], device=dev)
+    dist.all_reduce(t)
+    buf.close()
+    dist.destroy_process_group()
+    if rank == 0:
+        print(f"multi-GPU parity: world={P} failures={int(t.item())}", flush=True)
+    return 0 if int(t.item()) == 0 else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

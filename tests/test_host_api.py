@@ -1,0 +1,158 @@
+"""Host-side logic (CPU only): the routing/topology/balancer mirrors agree
+with the reference's golden inputs and known answers, and the C-ABI library
+loads and exports every symbol include/fusco.h declares."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden_names, load_golden
+from paper_2512_22036_b200 import balancer as B
+from paper_2512_22036_b200 import routing as R
+from paper_2512_22036_b200 import topology as T
+
+GEN_OF = {
+    "box2_e8k2_uniform": ("realworld", {"zipf_s": 0.0}, 0),
+    "box8_e256k8_zipf": ("realworld", {"zipf_s": 1.2}, 0),
+    "box8_e64k8_scaled": ("realworld", {"zipf_s": 1.1}, 2),
+    "box4_single_node": ("single_node", {"remote_only": True}, 4),
+    "grid4x4_e32k4": ("realworld", {}, 3),
+    "grid2x2_imbalanced": ("imbalanced", {}, 5),
+    "box1_degenerate": ("realworld", {}, 6),
+    "box3_ragged_tb12": ("realworld", {"zipf_s": 0.5}, 7),
+}
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_generators_reproduce_reference_routing(name):
+    g = load_golden(name)
+    gen, kw, seed = GEN_OF[name]
+    topo = T.ClusterTopology(g["num_nodes"], g["gpus_per_node"])
+    pl = T.round_robin_placement(g["num_experts"], topo)
+    a = R.GENERATORS[gen](g["experts"].shape[0], g["topk"], topo, pl, seed=seed, **kw)
+    assert np.array_equal(a.experts, g["experts"])
+    assert np.array_equal(a.weights, g["weights"])
+    assert np.array_equal(a.source, g["source"])
+    assert np.array_equal(pl.owner, g["owner"])
+    assert np.array_equal(R.derive_token_node(a, pl, topo).first_mask, g["first_mask"])
+
+
+def test_routing_validation_errors():
+    with pytest.raises(ValueError):
+        R.RoutingAssignment(1, 2, np.array([[3, 3]]), np.array([[0.5, 0.5]]), np.array([0]))
+    with pytest.raises(ValueError):
+        R.RoutingAssignment(1, 2, np.array([[1, 3]]), np.array([[0.7, 0.5]]), np.array([0]))
+    with pytest.raises(ValueError):
+        R.RoutingAssignment(1, 1, np.array([[-1]]), np.array([[1.0]]), np.array([0]))
+
+
+def test_local_routing_and_sources():
+    topo = T.box(4)
+    pl = T.round_robin_placement(16, topo)
+    a = R.gen_realworld(40, 2, topo, pl, seed=1)
+    assert a.source.tolist() == [t % 4 for t in range(40)]
+    ids, idx, w = R.local_routing(a, 2)
+    assert ids.tolist() == list(range(2, 40, 4))
+    assert np.array_equal(idx, a.experts[ids]) and np.array_equal(w, a.weights[ids])
+
+
+def test_trace_round_trip(tmp_path):
+    topo = T.box(2)
+    pl = T.round_robin_placement(8, topo)
+    a = R.gen_realworld(10, 2, topo, pl, seed=0)
+    R.save_trace(tmp_path / "t.json", a, 64)
+    b, tb = R.load_trace(tmp_path / "t.json")
+    assert tb == 64 and np.array_equal(a.experts, b.experts) and np.array_equal(a.weights, b.weights)
+
+
+def test_balancer_worked_example_and_rotation():
+    """Reference test_balancer.py:49-57 (minimax 7) and heaviest GPU of node n in group n % M."""
+    topo = T.ClusterTopology(2, 2)
+    loads = np.array([[5, 3], [4, 1]])
+    g = B.greedy_groups(loads, topo)
+    assert B.group_load(loads, g, topo).max() == 7
+    _, best = B.optimal_groups(loads, topo)
+    assert best == 7
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        topo = T.ClusterTopology(3, 4)
+        L = rng.integers(0, 100, size=(3, 4))
+        g = B.greedy_groups(L, topo)
+        B.validate_groups(g, topo)
+        for n in range(3):
+            assert g[n, n % 4] == int(np.argsort(-L[n], kind="stable")[0])
+    # inside one box (M = 1) the group table is trivial
+    assert np.array_equal(B.greedy_groups(np.arange(8), T.box(8)), np.zeros((8, 1), dtype=np.int64))
+
+
+def test_topology_json_and_presets(tmp_path):
+    topo, pl = T.preset("large")
+    assert topo.num_gpus == 64 and np.bincount(pl.owner).tolist() == [4] * 64
+    T.save_topology(tmp_path / "t.json", topo, pl)
+    t2, p2 = T.load_topology(tmp_path / "t.json")
+    assert t2 == topo and np.array_equal(p2.owner, pl.owner)
+    with pytest.raises(ValueError):
+        T.ClusterTopology(0, 1)
+
+
+# ---- the C-ABI library -------------------------------------------------------
+
+HEADER = ROOT / "include" / "fusco.h"
+
+
+def header_symbols():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(fs_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2512_22036_b200 import _lib
+
+    lib = _lib.load()
+    syms = header_symbols()
+    assert len(syms) >= 18
+    for s in syms:
+        assert hasattr(lib, s), s
+        assert s in _lib.SIGNATURES, f"{s} missing a ctypes signature"
+    assert lib.fs_abi_version() == 1
+
+
+def test_library_validates_before_touching_cuda():
+    """Argument errors come back as ValueError without needing a GPU."""
+    from ctypes import byref, c_size_t, c_void_p
+
+    from paper_2512_22036_b200 import _lib
+
+    n = c_size_t()
+    _lib.call("fs_region_bytes", 8, 256, 14336, 1000, 1, byref(n))
+    # signal block + 2x counts + 2x fan_src + 3x rows
+    assert n.value >= 4096 + 3 * 1000 * 14336
+    with pytest.raises(ValueError):
+        _lib.call("fs_region_bytes", 0, 256, 14336, 1000, 1, byref(n))
+    owner = (np.arange(8) % 2).astype(np.int32)
+    peers = (c_void_p * 2)(1, 2)
+    h = c_void_p()
+    with pytest.raises(ValueError):  # topk > num_experts
+        _lib.call("fs_create", 0, 0, 2, 8, 9, 64, 16, 0, 0, owner.ctypes.data_as(c_void_p), None, peers, 0, 0,
+                  byref(h))
+    with pytest.raises(ValueError):  # token_bytes not a multiple of 4
+        _lib.call("fs_create", 0, 0, 2, 8, 2, 66, 16, 0, 0, owner.ctypes.data_as(c_void_p), None, peers, 0, 0,
+                  byref(h))
+    bad_owner = np.full(8, 5, dtype=np.int32)
+    with pytest.raises(ValueError):  # owner outside [0, world)
+        _lib.call("fs_create", 0, 0, 2, 8, 2, 64, 16, 0, 0, bad_owner.ctypes.data_as(c_void_p), None, peers, 0, 0,
+                  byref(h))
+    with pytest.raises(ValueError):
+        _lib.call("fs_layout", None, None, 4, 0, None, None, None, None, None, None, 3, None)
+    assert "null handle" in _lib.load().fs_last_error().decode()
+
+
+def test_no_cpu_fallback_in_product_path():
+    """The product package never imports the oracle (test infrastructure)."""
+    pkg = ROOT / "paper_2512_22036_b200"
+    for py in pkg.rglob("*.py"):
+        src = py.read_text()
+        assert "import oracle" not in src and "from oracle" not in src, py
