@@ -16,7 +16,7 @@ using namespace fusco;
 
 namespace {
 
-constexpr int kMaxCtasPerSm = 4;
+constexpr int kMaxCtasPerSm = 8;
 thread_local std::string g_err;
 
 int fail(int code, const std::string& msg) {
@@ -59,6 +59,9 @@ struct fs_ctx {
   int nloc;
   int layout_grid_max;  // cooperative capacity of the layout kernel
   int move_grid;        // dispatch persistent grid (equal on all ranks)
+  int dispatch_tma;     // 1: TMA bulk-copy dispatch engine (FUSCO_DISPATCH=tma)
+  int tma_slots;        // smem ring slots per CTA of the TMA engine
+  size_t tma_smem;
   int sms;
   int combine_grid_cap; // 0 = occupancy-derived
   size_t layout_smem;
@@ -70,6 +73,7 @@ struct fs_ctx {
   long long* stat_part_d;
   int* status_d;
   int* num_rows_d;
+  uint32_t* epoch_d;  // device iteration counter (graph-replay safe)
 };
 
 namespace {
@@ -84,8 +88,7 @@ FsArgs make_args(const fs_ctx* h, int T, int idx64) {
   a.tb = h->tb;
   a.T = T;
   a.idx64 = idx64;
-  a.epoch = h->epoch;
-  a.parity = (int)(h->epoch & 1u);
+  a.epoch_ptr = h->epoch_d;
   a.max_rows = h->max_rows;
   a.owner = h->owner_d;
   a.node_of = h->node_of_d;
@@ -264,6 +267,23 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
   if ((rc = occupancy(dispatch_kernel<int>, kMoveThreads, 0, &o))) return cleanup(rc);
   occ_d = std::max(1, std::min(std::min(occ_d, o), kMaxCtasPerSm));
   h->move_grid = grid_ctas > 0 ? std::min(grid_ctas, occ_d * sms) : occ_d * sms;
+  // TMA engine: ~100 KB of row slots per CTA, two CTAs per SM
+  {
+    const char* mode = getenv("FUSCO_DISPATCH");
+    h->dispatch_tma = (mode && std::string(mode) == "tma" && token_bytes % 16 == 0) ? 1 : 0;
+    const int slot = tma_slot_bytes(token_bytes);
+    h->tma_slots = std::max(2, std::min(kTmaMaxSlots, (int)((100 * 1024 - 512) / slot)));
+    h->tma_smem = 2 * kTmaMaxSlots * sizeof(uint64_t) + (size_t)h->tma_slots * slot;
+    if (h->dispatch_tma) {
+      if (h->tma_smem > 227 * 1024) return cleanup(fail(FS_EINVAL, "token too large for the TMA engine"));
+      e = cudaFuncSetAttribute(dispatch_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tma_smem);
+      if (e != cudaSuccess) return cleanup(fail(FS_ECUDA, cudaGetErrorString(e)));
+      int occ_t = 0;
+      if ((rc = occupancy(dispatch_tma_kernel, kTmaThreads, h->tma_smem, &occ_t))) return cleanup(rc);
+      occ_t = std::max(1, std::min(occ_t, 2));
+      h->move_grid = grid_ctas > 0 ? std::min(grid_ctas, occ_t * sms) : occ_t * sms;
+    }
+  }
   h->sms = sms;
   h->combine_grid_cap = grid_ctas > 0 ? grid_ctas : 0;
 
@@ -275,7 +295,8 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
       (e = dalloc((void**)&h->chunk_cnt_d, (size_t)max_chunks * num_experts * 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->stat_part_d, (size_t)h->layout_grid_max * 8 * 8)) != cudaSuccess ||
       (e = dalloc((void**)&h->status_d, 4)) != cudaSuccess ||
-      (e = dalloc((void**)&h->num_rows_d, 4)) != cudaSuccess)
+      (e = dalloc((void**)&h->num_rows_d, 4)) != cudaSuccess ||
+      (e = dalloc((void**)&h->epoch_d, 4)) != cudaSuccess)
     return cleanup(fail(FS_ECUDA, std::string("fs_create alloc: ") + cudaGetErrorString(e)));
   if ((e = cudaMemcpy(h->owner_d, owner.data(), num_experts * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(h->node_of_d, nodes.data(), world * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
@@ -283,6 +304,7 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
       (e = cudaMemcpy(h->seg_d, seg.data(), (world + 1) * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemset(h->status_d, 0, 4)) != cudaSuccess ||
       (e = cudaMemset(h->num_rows_d, 0, 4)) != cudaSuccess ||
+      (e = cudaMemset(h->epoch_d, 0, 4)) != cudaSuccess ||
       (e = cudaDeviceSynchronize()) != cudaSuccess)
     return cleanup(fail(FS_ECUDA, std::string("fs_create init: ") + cudaGetErrorString(e)));
   *out = h;
@@ -300,6 +322,7 @@ int fs_destroy(fs_handle_t h) {
   cudaFree(h->stat_part_d);
   cudaFree(h->status_d);
   cudaFree(h->num_rows_d);
+  cudaFree(h->epoch_d);
   delete h;
   return FS_OK;
 }
@@ -369,6 +392,14 @@ int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_byte
   FsArgs a = make_args(h, num_tokens, idx_bytes == 8);
   const bool vec16 = (h->tb % 16 == 0) && aligned(x, 16);
   if (!aligned(x, 4)) return fail(FS_EINVAL, "x must be 4-byte aligned");
+  if (h->dispatch_tma) {
+    if (!vec16) return fail(FS_EINVAL, "TMA dispatch needs 16-byte aligned rows");
+    int nslots = h->tma_slots;
+    void* targs[] = {&a, (void*)&x, (void*)&topk_idx, (void*)&row_of, &phase, &nslots};
+    FS_CUDA(cudaLaunchCooperativeKernel((const void*)dispatch_tma_kernel, dim3(h->move_grid), dim3(kTmaThreads),
+                                        targs, h->tma_smem, (cudaStream_t)stream));
+    return FS_OK;
+  }
   void* args[] = {&a, (void*)&x, (void*)&topk_idx, (void*)&row_of, &phase};
   const void* fn = vec16 ? (const void*)dispatch_kernel<int4> : (const void*)dispatch_kernel<int>;
   // fixed grid: receivers expect epoch * world * move_grid arrival signals

@@ -29,8 +29,11 @@ constexpr size_t kOffArrive = 512;     // u64: dispatch CTAs that finished pushi
 struct FsArgs {
   int rank, world, E, K, tb, T;
   int idx64;      // topk_idx element size 8 (else 4)
-  int parity;     // epoch & 1: which act / count / fan_src copy
-  uint32_t epoch;
+  // Iteration counter in device memory (per handle), so a captured CUDA graph
+  // replays correctly: fs_layout's LOCAL phase uses *epoch + 1 and stores it;
+  // every later phase/kernel of the iteration reads it.  parity = epoch & 1
+  // selects the act / count / fan_src copy.
+  uint32_t* epoch_ptr;
   long long max_rows;
   const int32_t* owner;      // [E] expert -> rank
   const int32_t* node_of;    // [P] rank -> node (first_mask statistics)
@@ -157,9 +160,68 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
   return v;
 }
 
+__device__ __forceinline__ uint32_t load_epoch(const FsArgs& a) {
+  return *reinterpret_cast<volatile const uint32_t*>(a.epoch_ptr);
+}
+
 __device__ __forceinline__ long long load_idx(const void* idx, size_t pos, int idx64) {
   return idx64 ? reinterpret_cast<const long long*>(idx)[pos]
                : (long long)reinterpret_cast<const int32_t*>(idx)[pos];
+}
+
+// ---- mbarrier + bulk-copy (TMA) primitives --------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared (this CTA), completion counted on an mbarrier
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// shared -> global (local HBM or a peer's HBM over NVLink), bulk-group tracked
+__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 }  // namespace fusco

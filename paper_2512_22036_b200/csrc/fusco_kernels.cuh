@@ -57,6 +57,8 @@ __global__ void __launch_bounds__(kLayoutThreads)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nchunks = (T + kLayoutThreads - 1) / kLayoutThreads;
   const uint32_t lt_mask = (1u << lane) - 1u;
+  const uint32_t epoch = load_epoch(a) + ((phase & FS_PHASE_LOCAL) ? 1u : 0u);
+  const int parity = (int)(epoch & 1u);
 
   if (phase & FS_PHASE_LOCAL) {
     uint32_t* bits = sm;                       // [8][E]
@@ -127,30 +129,28 @@ __global__ void __launch_bounds__(kLayoutThreads)
     }
     grid.sync();
 
-    // Exclusive scan of every expert's chunk counts (one warp per expert),
-    // then publish this rank's per-expert totals into every peer's count
-    // matrix row [s] (the 8 KB "all-gather" of the P x E count matrix).
-    const int gw = blockIdx.x * kLayoutWarps + warp, nw = gridDim.x * kLayoutWarps;
-    for (int e = gw; e < E; e += nw) {
-      int run = 0;
-      for (int cb = 0; cb < nchunks; cb += 32) {
-        const int c = cb + lane;
-        const int val = c < nchunks ? a.chunk_cnt[(size_t)c * E + e] : 0;
-        const int incl = warp_incl_scan(val, lane);
-        if (c < nchunks) a.chunk_cnt[(size_t)c * E + e] = run + incl - val;
-        run += __shfl_sync(kFull, incl, 31);
-      }
-      for (int g = lane; g < P; g += 32) {
-        int32_t* dst = reinterpret_cast<int32_t*>(a.peer[g] + a.off_count +
-                                                  (size_t)a.parity * a.count_stride);
-        dst[(size_t)s * E + e] = run;
-      }
-    }
-    __threadfence_system();
-    grid.sync();
+    // One CTA turns the chunk counts into per-chunk exclusive offsets and
+    // publishes this rank's per-expert totals into every peer's count matrix
+    // row [s] (the P x E count all-gather, 8 KB at P=8, E=256) — then a single
+    // release store per peer.  Only one grid-wide barrier in the kernel.
     if (blockIdx.x == 0) {
-      if (tid < P)
-        st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[tid] + kOffCountFlag) + s, a.epoch);
+      for (int e = tid; e < E; e += kLayoutThreads) {
+        int run = 0;
+        for (int c0 = 0; c0 < nchunks; c0 += 8) {
+          int v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = (c0 + j < nchunks) ? a.chunk_cnt[(size_t)(c0 + j) * E + e] : 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (c0 + j < nchunks) a.chunk_cnt[(size_t)(c0 + j) * E + e] = run;
+            run += v[j];
+          }
+        }
+        for (int g = 0; g < P; ++g) {
+          int32_t* dst = reinterpret_cast<int32_t*>(a.peer[g] + a.off_count + (size_t)parity * a.count_stride);
+          dst[(size_t)s * E + e] = run;
+        }
+      }
       if (stats && tid < 4) {
         long long acc = 0;
         for (int b = 0; b < (int)gridDim.x; ++b) acc += a.stat_part[b * 8 + tid];
@@ -159,18 +159,25 @@ __global__ void __launch_bounds__(kLayoutThreads)
         stats[slot[tid]] = acc;
       }
       if (stats && tid >= 5 && tid < FS_NSTATS) stats[tid] = 0;
+      // every CTA read the old epoch before the grid barrier: safe to bump
+      if (tid == 0) *a.epoch_ptr = epoch;
+      __syncthreads();
+      // release: the count rows (and the chunk offsets other CTAs of this rank
+      // read after acquiring their own flag) happen-before these stores
+      if (tid < P)
+        st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[tid] + kOffCountFlag) + s, epoch);
     }
   }
 
   if (phase & FS_PHASE_REMOTE) {
     if (tid < P)
-      wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffCountFlag) + tid, a.epoch, a);
+      wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffCountFlag) + tid, epoch, a);
     __syncthreads();
     int32_t* tot = reinterpret_cast<int32_t*>(sm);
     int32_t* base = tot + E;
     int32_t* before = base + E;
     const int32_t* cnt =
-        reinterpret_cast<const int32_t*>(a.peer[s] + a.off_count + (size_t)a.parity * a.count_stride);
+        reinterpret_cast<const int32_t*>(a.peer[s] + a.off_count + (size_t)parity * a.count_stride);
     for (int e = tid; e < E; e += kLayoutThreads) {
       int t = 0, b = 0;
       for (int q = 0; q < P; ++q) {
@@ -245,7 +252,7 @@ __global__ void __launch_bounds__(kLayoutThreads)
 // ===========================================================================
 template <typename V>
 struct MoveCfg {
-  static constexpr int U = sizeof(V) == 16 ? 4 : 8;  // words per lane per unit
+  static constexpr int U = sizeof(V) == 16 ? 8 : 16;  // words per lane per unit (4 KB / 2 KB)
   static constexpr int kSliceWords = 32 * U;
 };
 
@@ -280,8 +287,10 @@ __global__ void __launch_bounds__(kMoveThreads)
   const int lane = threadIdx.x & 31;
   const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nw = (int)((gridDim.x * blockDim.x) >> 5);
-  const size_t act_off = a.off_act + (size_t)a.parity * a.act_stride;
-  const size_t fan_off = a.off_fansrc + (size_t)a.parity * a.fansrc_stride;
+  const uint32_t epoch = load_epoch(a);
+  const int parity = (int)(epoch & 1u);
+  const size_t act_off = a.off_act + (size_t)parity * a.act_stride;
+  const size_t fan_off = a.off_fansrc + (size_t)parity * a.fansrc_stride;
 
   if (phase & FS_PHASE_LOCAL) {
     const long long units = (long long)T * S;
@@ -333,17 +342,19 @@ __global__ void __launch_bounds__(kMoveThreads)
         }
       }
     }
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x < P)
-      red_release_sys_add_u64(
-          reinterpret_cast<unsigned long long*>(a.peer[threadIdx.x] + kOffArrive), 1ull);
+    if (P > 1) {
+      // release (cumulative over the CTA's stores via bar.sync) per peer
+      __syncthreads();
+      if (threadIdx.x < P)
+        red_release_sys_add_u64(
+            reinterpret_cast<unsigned long long*>(a.peer[threadIdx.x] + kOffArrive), 1ull);
+    }
   }
 
   if ((phase & FS_PHASE_REMOTE) && P > 1) {
     if (threadIdx.x == 0)
       wait_u64_geq(reinterpret_cast<const unsigned long long*>(a.peer[s] + kOffArrive),
-                   (unsigned long long)a.epoch * (unsigned long long)P * gridDim.x, a);
+                   (unsigned long long)epoch * (unsigned long long)P * gridDim.x, a);
     __syncthreads();
     const int rows = *reinterpret_cast<volatile int*>(a.num_rows);
     const int32_t* fs = reinterpret_cast<const int32_t*>(a.peer[s] + fan_off);
@@ -352,6 +363,127 @@ __global__ void __launch_bounds__(kMoveThreads)
       const int r = r0 + lane;
       const int f = r < rows ? ld_cg(fs + r) : r;
       uint32_t need = __ballot_sync(kFull, r < rows && f != r && f >= 0 && f < rows);
+      while (need) {
+        const int d = __ffs(need) - 1;
+        need &= need - 1;
+        const int ff = __shfl_sync(kFull, f, d);
+        warp_copy_row_cg(act + (size_t)(r0 + d) * nv, act + (size_t)ff * nv, nv, lane);
+      }
+    }
+  }
+}
+
+// ===========================================================================
+// Dispatch, TMA engine
+//
+// Same protocol and outputs as dispatch_kernel, different data mover: per
+// CTA a ring of NS shared-memory row slots.  Warp 0 (one elected thread)
+// streams whole token rows global->shared with cp.async.bulk, completion on
+// a per-slot mbarrier (expect_tx).  Warp 1 resolves the token's destinations
+// (same per-rank dedup as above) and one lane issues one cp.async.bulk
+// shared->global store per destination row — local HBM or a peer's HBM over
+// NVLink — committing one bulk group per token; a slot is handed back to the
+// producer once its group has finished reading shared memory
+// (wait_group.read with a lag).  The registers never hold payload: bytes in
+// flight per SM are NS rows, independent of occupancy.
+// ===========================================================================
+constexpr int kTmaThreads = 128;
+constexpr int kTmaMaxSlots = 32;
+constexpr int kTmaLag = 2;  // bulk groups allowed to still be reading smem
+
+__host__ __device__ inline int tma_slot_bytes(int tb) { return (tb + 127) & ~127; }
+
+__global__ void __launch_bounds__(kTmaThreads)
+    dispatch_tma_kernel(FsArgs a, const char* __restrict__ x, const void* __restrict__ idx,
+                        const int32_t* __restrict__ row_of, int phase, int nslots) {
+  extern __shared__ __align__(128) char tsm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
+  uint64_t* empty = full + kTmaMaxSlots;
+  char* ring = tsm + 2 * kTmaMaxSlots * sizeof(uint64_t);
+  const int K = a.K, T = a.T, P = a.world, s = a.rank, tb = a.tb;
+  const int slot_bytes = tma_slot_bytes(tb);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t epoch = load_epoch(a);
+  const int parity = (int)(epoch & 1u);
+  const size_t act_off = a.off_act + (size_t)parity * a.act_stride;
+  const size_t fan_off = a.off_fansrc + (size_t)parity * a.fansrc_stride;
+
+  if (phase & FS_PHASE_LOCAL) {
+    if (threadIdx.x == 0) {
+      for (int q = 0; q < nslots; ++q) {
+        mbar_init(&full[q], 1);
+        mbar_init(&empty[q], 1);
+      }
+      mbar_fence_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+      if (lane == 0) {  // producer
+        int n = 0;
+        for (int i = blockIdx.x; i < T; i += gridDim.x, ++n) {
+          const int q = n % nslots;
+          if (n >= nslots) mbar_wait(&empty[q], ((n / nslots) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[q], (uint32_t)tb);
+          bulk_load(ring + (size_t)q * slot_bytes, x + (size_t)i * tb, (uint32_t)tb, &full[q]);
+        }
+      }
+    } else if (warp == 1) {  // destinations + bulk stores
+      int n = 0;
+      for (int i = blockIdx.x; i < T; i += gridDim.x, ++n) {
+        const int q = n % nslots;
+        int g = -1 - lane, r = -1;
+        if (lane < K) {
+          long long e = load_idx(idx, (size_t)i * K + lane, a.idx64);
+          if (e < 0 || e >= a.E) e = 0;
+          g = a.owner[e];
+          r = row_of[(size_t)i * K + lane];
+          if (r < 0 || r >= a.max_rows) r = -1;
+        }
+        const uint32_t same = __match_any_sync(kFull, g);
+        const int first_lane = __ffs(same) - 1;
+        const int r_first = __shfl_sync(kFull, r, first_lane);
+        const bool direct = lane < K && r >= 0 && (first_lane == lane || g == s);
+        if (lane < K && r >= 0) {
+          int32_t* fs = reinterpret_cast<int32_t*>(a.peer[g] + fan_off);
+          fs[r] = direct ? r : r_first;
+        }
+        mbar_wait(&full[q], (n / nslots) & 1);
+        // each destination lane issues its own bulk store (per-thread bulk
+        // groups); every lane commits one group per token so the lag below
+        // counts tokens on all lanes
+        if (direct)
+          bulk_store(a.peer[g] + act_off + (size_t)r * tb, ring + (size_t)q * slot_bytes, (uint32_t)tb);
+        bulk_commit();
+        bulk_wait_read<kTmaLag>();
+        __syncwarp();
+        if (lane == 0 && n >= kTmaLag) mbar_arrive(&empty[(n - kTmaLag) % nslots]);
+      }
+      bulk_wait<0>();
+      fence_proxy_async_global();
+    }
+    if (P > 1) {
+      __syncthreads();
+      if (threadIdx.x < P)
+        red_release_sys_add_u64(
+            reinterpret_cast<unsigned long long*>(a.peer[threadIdx.x] + kOffArrive), 1ull);
+    }
+  }
+
+  if ((phase & FS_PHASE_REMOTE) && P > 1) {
+    if (threadIdx.x == 0)
+      wait_u64_geq(reinterpret_cast<const unsigned long long*>(a.peer[s] + kOffArrive),
+                   (unsigned long long)epoch * (unsigned long long)P * gridDim.x, a);
+    __syncthreads();
+    const int rows = *reinterpret_cast<volatile int*>(a.num_rows);
+    const int nv = tb / 16;
+    const int32_t* fs = reinterpret_cast<const int32_t*>(a.peer[s] + fan_off);
+    int4* act = reinterpret_cast<int4*>(a.peer[s] + act_off);
+    const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+    for (int r0 = gw * 32; r0 < rows; r0 += nw * 32) {
+      const int rr = r0 + lane;
+      const int f = rr < rows ? ld_cg(fs + rr) : rr;
+      uint32_t need = __ballot_sync(kFull, rr < rows && f != rr && f >= 0 && f < rows);
       while (need) {
         const int d = __ffs(need) - 1;
         need &= need - 1;
@@ -411,7 +543,7 @@ __global__ void __launch_bounds__(kMoveThreads)
                    int phase) {
   using Acc = typename std::conditional<ACC64, double, float>::type;
   using EL = Elem<V, BF16>;
-  constexpr int U = sizeof(V) == 16 ? 2 : 4;  // words per lane per unit
+  constexpr int U = sizeof(V) == 16 ? 4 : 8;  // words per lane per unit
   constexpr int SW = 32 * U;
   constexpr int KG = 4;                       // experts whose loads are in flight together
   const int K = a.K, T = a.T, P = a.world, s = a.rank;
@@ -420,20 +552,19 @@ __global__ void __launch_bounds__(kMoveThreads)
   const int lane = threadIdx.x & 31;
   const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  const uint32_t epoch = load_epoch(a);
   const size_t src_off =
-      src_sel == FS_SRC_ACT_OUT ? a.off_actout : a.off_act + (size_t)a.parity * a.act_stride;
+      src_sel == FS_SRC_ACT_OUT ? a.off_actout : a.off_act + (size_t)(epoch & 1u) * a.act_stride;
 
   if (phase & FS_PHASE_LOCAL) {
     if (blockIdx.x == 0 && threadIdx.x < P) {
       __threadfence_system();
-      st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[threadIdx.x] + kOffReadyFlag) + s,
-                         a.epoch);
+      st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[threadIdx.x] + kOffReadyFlag) + s, epoch);
     }
   }
   if (phase & FS_PHASE_REMOTE) {
     if (threadIdx.x < P)
-      wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffReadyFlag) + threadIdx.x,
-                   a.epoch, a);
+      wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffReadyFlag) + threadIdx.x, epoch, a);
     __syncthreads();
     const long long units = (long long)T * S;
     for (long long u = gw; u < units; u += nw) {

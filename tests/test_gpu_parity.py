@@ -191,6 +191,34 @@ def test_bf16_parity_with_oracle(P, E, K, T_l, hidden, zipf):
         np.testing.assert_allclose(got, want, **BF16_TOL)
 
 
+@pytest.fixture
+def tma_dispatch(monkeypatch):
+    """Select the TMA bulk-copy dispatch engine for handles created in the test."""
+    monkeypatch.setenv("FUSCO_DISPATCH", "tma")
+    yield
+
+
+@pytest.mark.parametrize(
+    "P,E,K,T_l,hidden,zipf",
+    [
+        (8, 256, 8, 128, 7168, 1.2),
+        (4, 8, 2, 1024, 4096, 0.0),
+        (1, 8, 2, 2048, 4096, 0.0),
+        (2, 16, 4, 333, 1024, 0.3),
+    ],
+)
+def test_tma_dispatch_parity_with_oracle(tma_dispatch, P, E, K, T_l, hidden, zipf):
+    pkg, topo, pl, a, tb, payload = _cluster_case(P, E, K, T_l, hidden, "bf16", zipf, seed=P * 5 + K)
+    res = _run_cluster(pkg, topo, pl, a, tb, payload, "bf16", "f64")
+    layouts, row_of = _check_layout(res, a, pl, P)
+    acts = O.dispatch(payload, layouts)
+    for g in range(P):
+        assert np.array_equal(res["acts"][g], acts[g]), f"activation/{g}"
+    for s in range(P):
+        want = O.combine(acts, row_of, a.experts, a.weights, pl.owner, res["ids"][s], "bf16")
+        assert np.array_equal(res["outs"][s], want)
+
+
 def test_repeated_epochs_reuse_buffers():
     """Four consecutive shuffles on one cluster (epoch parity flips the
     double-buffered activation/count/fan-out regions)."""
