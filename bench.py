@@ -150,6 +150,8 @@ def parse():
     ap.add_argument("--graph", action="store_true", help="time K steps as CUDA-graph replays")
     ap.add_argument("--dispatch", choices=["warp", "tma"], default=os.environ.get("FUSCO_DISPATCH", "warp"),
                     help="dispatch data mover: warp LDG/STG loop or TMA bulk copies")
+    ap.add_argument("--combine", choices=["warp", "tma"], default=os.environ.get("FUSCO_COMBINE", "warp"),
+                    help="combine data mover: warp LDG loop or TMA bulk loads into smem stages")
     return ap.parse_args()
 
 
@@ -248,6 +250,7 @@ def main() -> int:
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
 
     os.environ["FUSCO_DISPATCH"] = args.dispatch
+    os.environ["FUSCO_COMBINE"] = args.combine
     buf = EPBuffer(num_experts=E, topk=K, hidden=hidden, dtype=dtype, max_tokens=T_l, with_act_out=False)
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
     NSET = 2  # rotate input/output sets so consecutive steps touch different memory (L2 126 MB)
@@ -478,6 +481,7 @@ def main() -> int:
         "gpu_launches": launches,
         "launch_mode": "cuda_graph" if graph is not None else "eager",
         "dispatch_engine": args.dispatch,
+        "combine_engine": args.combine,
         "host_enqueue_ms_per_step": host_ms / args.steps,
         "clocks": clocks,
     }

@@ -77,6 +77,22 @@ extern "C" {
 #define FS_STAT_NODE_DEDUP 4    /* Σ_t |distinct remote nodes of t| = dispatch_loads/tb */
 #define FS_NSTATS 8
 
+/* trace slots (globaltimer ns, CTA 0 thread 0) when created with FUSCO_TRACE=1 */
+#define FS_TRACE_LAYOUT_BEGIN 0
+#define FS_TRACE_LAYOUT_HIST 1
+#define FS_TRACE_LAYOUT_GRIDSYNC 2
+#define FS_TRACE_LAYOUT_PUBLISH 3
+#define FS_TRACE_LAYOUT_WAIT 4
+#define FS_TRACE_LAYOUT_END 5
+#define FS_TRACE_DISPATCH_BEGIN 8
+#define FS_TRACE_DISPATCH_PUSHED 9
+#define FS_TRACE_DISPATCH_ARRIVED 10
+#define FS_TRACE_DISPATCH_END 11
+#define FS_TRACE_COMBINE_BEGIN 12
+#define FS_TRACE_COMBINE_READY 13
+#define FS_TRACE_COMBINE_END 14
+#define FS_NTRACE 16
+
 typedef struct fs_ctx* fs_handle_t;
 
 int fs_abi_version(void);
@@ -159,6 +175,11 @@ int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes,
 /* Synchronise the stream and return the device status word (FS_OK, or the
  * first FS_ETIMEOUT / FS_ERANGE a kernel recorded); clears it. */
 int fs_check(fs_handle_t h, void* stream);
+
+/* Copy the trace stamps (FS_NTRACE u64, 0 when never written) to host
+ * memory; synchronises the stream.  FS_EINVAL unless created with
+ * FUSCO_TRACE=1 in the environment. */
+int fs_trace(fs_handle_t h, uint64_t* host_out, void* stream);
 
 /* P2P/HBM copy-bandwidth probe: copies `bytes` from src to dst with the
  * same 16-byte warp copy loop the engine uses (used by bench.py to measure

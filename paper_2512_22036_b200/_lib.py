@@ -59,6 +59,7 @@ SIGNATURES = {
          c_int, c_void_p],
     ),
     "fs_check": (c_int, [c_void_p, c_void_p]),
+    "fs_trace": (c_int, [c_void_p, c_void_p, c_void_p]),
     "fs_probe_copy": (c_int, [c_int, c_void_p, c_void_p, c_size_t, c_int, c_void_p]),
 }
 

@@ -62,6 +62,9 @@ struct fs_ctx {
   int dispatch_tma;     // 1: TMA bulk-copy dispatch engine (FUSCO_DISPATCH=tma)
   int tma_slots;        // smem ring slots per CTA of the TMA engine
   size_t tma_smem;
+  int combine_tma;      // 1: TMA combine engine (FUSCO_COMBINE=tma)
+  int comb_sb, comb_stages, comb_grid;
+  size_t comb_smem;
   int sms;
   int combine_grid_cap; // 0 = occupancy-derived
   size_t layout_smem;
@@ -69,11 +72,12 @@ struct fs_ctx {
   unsigned long long timeout_ns;
   RegionLayout L;
   std::vector<char*> peers;
-  int32_t *owner_d, *node_of_d, *perm_d, *seg_d, *chunk_cnt_d;
+  int32_t *owner_d, *node_of_d, *perm_d, *seg_d, *chunk_cnt_d, *totals_d;
   long long* stat_part_d;
   int* status_d;
   int* num_rows_d;
   uint32_t* epoch_d;  // device iteration counter (graph-replay safe)
+  unsigned long long* trace_d;  // FS_NTRACE stamps when FUSCO_TRACE=1, else null
 };
 
 namespace {
@@ -103,10 +107,12 @@ FsArgs make_args(const fs_ctx* h, int T, int idx64) {
   a.fansrc_stride = h->L.fansrc_stride;
   a.act_stride = h->L.act_stride;
   a.chunk_cnt = h->chunk_cnt_d;
+  a.totals = h->totals_d;
   a.stat_part = h->stat_part_d;
   a.status = h->status_d;
   a.num_rows = h->num_rows_d;
   a.timeout_ns = h->timeout_ns;
+  a.trace = h->trace_d;
   return a;
 }
 
@@ -237,7 +243,7 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
   h->timeout_ns = (unsigned long long)(timeout_ms > 0 ? timeout_ms : 10000) * 1000000ull;
   h->L = region_layout(world, num_experts, token_bytes, max_rows, h->with_act_out);
   h->peers.assign((char* const*)peer_regions, (char* const*)peer_regions + world);
-  h->layout_smem = layout_smem_bytes(num_experts);
+  h->layout_smem = layout_smem_bytes(num_experts, topk);
   auto cleanup = [&](int rc) {
     fs_destroy(h);
     return rc;
@@ -285,6 +291,32 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
     }
   }
   h->sms = sms;
+  // TMA combine: ~100 KB of [K][slice] stages per CTA, two CTAs per SM
+  {
+    const char* mode = getenv("FUSCO_COMBINE");
+    h->combine_tma = (mode && std::string(mode) == "tma" && token_bytes % 16 == 0) ? 1 : 0;
+    h->comb_sb = comb_slice_bytes(token_bytes, topk);
+    const int stage = topk * h->comb_sb;
+    h->comb_stages = std::max(2, std::min(kCombMaxStages, (100 * 1024) / stage));
+    h->comb_smem = 2 * kCombMaxStages * sizeof(uint64_t) + (size_t)h->comb_stages * stage;
+    h->comb_grid = 0;
+    if (h->combine_tma) {
+      if (h->comb_smem > 227 * 1024) return cleanup(fail(FS_EINVAL, "token too large for the TMA combine"));
+      const void* fns[4] = {(const void*)combine_tma_kernel<false, false>, (const void*)combine_tma_kernel<false, true>,
+                            (const void*)combine_tma_kernel<true, false>, (const void*)combine_tma_kernel<true, true>};
+      int occ_c = 1 << 30;
+      for (const void* f : fns) {
+        e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->comb_smem);
+        if (e != cudaSuccess) return cleanup(fail(FS_ECUDA, cudaGetErrorString(e)));
+        int o2 = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, f, kCombThreads, h->comb_smem);
+        if (e != cudaSuccess) return cleanup(fail(FS_ECUDA, cudaGetErrorString(e)));
+        occ_c = std::min(occ_c, o2);
+      }
+      occ_c = std::max(1, std::min(occ_c, 2));
+      h->comb_grid = grid_ctas > 0 ? std::min(grid_ctas, occ_c * sms) : occ_c * sms;
+    }
+  }
   h->combine_grid_cap = grid_ctas > 0 ? grid_ctas : 0;
 
   auto dalloc = [&](void** p, size_t n) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(n, 16)); };
@@ -293,6 +325,7 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
       (e = dalloc((void**)&h->perm_d, num_experts * 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->seg_d, (world + 1) * 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->chunk_cnt_d, (size_t)max_chunks * num_experts * 4)) != cudaSuccess ||
+      (e = dalloc((void**)&h->totals_d, (size_t)2 * num_experts * 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->stat_part_d, (size_t)h->layout_grid_max * 8 * 8)) != cudaSuccess ||
       (e = dalloc((void**)&h->status_d, 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->num_rows_d, 4)) != cudaSuccess ||
@@ -305,8 +338,17 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
       (e = cudaMemset(h->status_d, 0, 4)) != cudaSuccess ||
       (e = cudaMemset(h->num_rows_d, 0, 4)) != cudaSuccess ||
       (e = cudaMemset(h->epoch_d, 0, 4)) != cudaSuccess ||
+      (e = cudaMemset(h->totals_d, 0, (size_t)2 * num_experts * 4)) != cudaSuccess ||
       (e = cudaDeviceSynchronize()) != cudaSuccess)
     return cleanup(fail(FS_ECUDA, std::string("fs_create init: ") + cudaGetErrorString(e)));
+  {
+    const char* tr = getenv("FUSCO_TRACE");
+    if (tr && std::string(tr) == "1") {
+      if ((e = cudaMalloc((void**)&h->trace_d, FS_NTRACE * 8)) != cudaSuccess ||
+          (e = cudaMemset(h->trace_d, 0, FS_NTRACE * 8)) != cudaSuccess)
+        return cleanup(fail(FS_ECUDA, cudaGetErrorString(e)));
+    }
+  }
   *out = h;
   return FS_OK;
 }
@@ -319,10 +361,12 @@ int fs_destroy(fs_handle_t h) {
   cudaFree(h->perm_d);
   cudaFree(h->seg_d);
   cudaFree(h->chunk_cnt_d);
+  cudaFree(h->totals_d);
   cudaFree(h->stat_part_d);
   cudaFree(h->status_d);
   cudaFree(h->num_rows_d);
   cudaFree(h->epoch_d);
+  if (h->trace_d) cudaFree(h->trace_d);
   delete h;
   return FS_OK;
 }
@@ -432,6 +476,15 @@ int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes, const int32_t
   void* args[] = {&a, (void*)&topk_idx, (void*)&row_of, (void*)&topk_w, &w64, &out, &src, &phase};
   const void* fn;
   const bool bf = dtype == FS_DTYPE_BF16, f64 = acc == FS_ACC_F64;
+  if (h->combine_tma && vec16) {
+    fn = bf ? (f64 ? (const void*)combine_tma_kernel<true, true> : (const void*)combine_tma_kernel<true, false>)
+            : (f64 ? (const void*)combine_tma_kernel<false, true> : (const void*)combine_tma_kernel<false, false>);
+    int ns = h->comb_stages, sb = h->comb_sb;
+    void* targs[] = {&a, (void*)&topk_idx, (void*)&row_of, (void*)&topk_w, &w64, &out, &src, &phase, &ns, &sb};
+    FS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(h->comb_grid), dim3(kCombThreads), targs, h->comb_smem,
+                                        (cudaStream_t)stream));
+    return FS_OK;
+  }
   if (vec16) {
     fn = bf ? (f64 ? (const void*)combine_kernel<int4, true, true> : (const void*)combine_kernel<int4, true, false>)
             : (f64 ? (const void*)combine_kernel<int4, false, true> : (const void*)combine_kernel<int4, false, false>);
@@ -459,6 +512,15 @@ int fs_check(fs_handle_t h, void* stream) {
   if (status == FS_ERANGE) return fail(FS_ERANGE, "routing out of range (expert id or row capacity)");
   if (status == FS_EINVAL) return fail(FS_EINVAL, "a token routes to the same expert twice");
   if (status != FS_OK) return fail(status, "device reported an error");
+  return FS_OK;
+}
+
+int fs_trace(fs_handle_t h, uint64_t* host_out, void* stream) {
+  if (!h || !host_out) return fail(FS_EINVAL, "null argument");
+  if (!h->trace_d) return fail(FS_EINVAL, "handle created without FUSCO_TRACE=1");
+  FS_CUDA(cudaSetDevice(h->device));
+  FS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  FS_CUDA(cudaMemcpy(host_out, h->trace_d, FS_NTRACE * 8, cudaMemcpyDeviceToHost));
   return FS_OK;
 }
 

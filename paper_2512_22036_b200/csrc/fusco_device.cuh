@@ -43,16 +43,23 @@ struct FsArgs {
   size_t off_count, off_fansrc, off_act, off_actout;
   size_t count_stride, fansrc_stride, act_stride;  // bytes per parity copy
   int32_t* chunk_cnt;        // [chunks][E] scratch (per handle)
+  int32_t* totals;           // [2][E] per-parity per-expert atomic totals (per handle)
   long long* stat_part;      // [layout grid][8] scratch
   int* status;               // first error code, FS_OK when clean
   int* num_rows;             // rows of the own activation buffer this epoch
   unsigned long long timeout_ns;
+  unsigned long long* trace;  // optional globaltimer stamps (FUSCO_TRACE=1), see FS_TRACE_*
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+
+// Phase timestamps written by CTA 0 / thread 0 when tracing is enabled.
+__device__ __forceinline__ void trace_stamp(const FsArgs& a, int slot) {
+  if (a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) a.trace[slot] = globaltimer();
 }
 
 __device__ __forceinline__ void record_error(int* status, int code) {

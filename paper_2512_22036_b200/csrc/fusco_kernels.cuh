@@ -24,12 +24,16 @@ constexpr int kLayoutThreads = 256;  // one token per thread per chunk
 constexpr int kLayoutWarps = kLayoutThreads / 32;
 constexpr int kMoveThreads = 256;    // dispatch / combine CTA size
 
-// Shared memory of the layout kernel: LOCAL needs two [8][E] bit tables,
-// REMOTE three [E] int tables.
-__host__ __device__ inline size_t layout_smem_bytes(int E) {
+// Shared memory of the layout kernel (bytes):
+//   owner table [E] + node table [32]
+//   LOCAL : bits[8][E] + wbase[8][E]            (REMOTE aliases: tot/base/before/pre [4][E])
+//   chunk : e_s[256*K] (expert ids of the chunk) + pos_s[256*K] (in-chunk positions)
+__host__ __device__ inline size_t layout_smem_bytes(int E, int K) {
+  const size_t tables = ((size_t)E + 32) * sizeof(int32_t);
   const size_t a = 2ull * kLayoutWarps * E * sizeof(uint32_t);
-  const size_t b = 3ull * E * sizeof(int32_t);
-  return a > b ? a : b;
+  const size_t b = 4ull * E * sizeof(int32_t);
+  const size_t chunk = 2ull * kLayoutThreads * K * sizeof(int32_t);
+  return tables + (a > b ? a : b) + chunk;
 }
 
 // ===========================================================================
@@ -42,7 +46,13 @@ __host__ __device__ inline size_t layout_smem_bytes(int E) {
 // The in-chunk position is computed without atomics on positions: each warp
 // ORs a lane bit into a per-(warp, expert) word; a token's rank among the
 // earlier tokens of its warp is popc(word & lanemask_lt), plus the sum of the
-// popcounts of the earlier warps.  Deterministic, hence bit-exact.
+// popcounts of the earlier warps.  Deterministic, hence bit-exact.  Per-expert
+// totals are accumulated with commutative atomics (exact integers), so one
+// CTA can publish them right after the single grid barrier.
+//
+// Global scratch per handle: chunk_cnt[chunks][E] (chunk counts), and
+// totals[2][E] (per-parity atomic accumulators; this epoch zeroes the other
+// parity for the next one).
 // ===========================================================================
 __global__ void __launch_bounds__(kLayoutThreads)
     layout_kernel(FsArgs a, const void* __restrict__ idx, int32_t* __restrict__ row_of,
@@ -59,40 +69,64 @@ __global__ void __launch_bounds__(kLayoutThreads)
   const uint32_t lt_mask = (1u << lane) - 1u;
   const uint32_t epoch = load_epoch(a) + ((phase & FS_PHASE_LOCAL) ? 1u : 0u);
   const int parity = (int)(epoch & 1u);
+  trace_stamp(a, FS_TRACE_LAYOUT_BEGIN);
+
+  int32_t* owner_s = reinterpret_cast<int32_t*>(sm);
+  int32_t* node_s = owner_s + E;
+  uint32_t* work = reinterpret_cast<uint32_t*>(node_s + 32);
+  const size_t work_words = (size_t)(2 * kLayoutWarps * E > 4 * E ? 2 * kLayoutWarps * E : 4 * E);
+  int32_t* e_s = reinterpret_cast<int32_t*>(work + work_words);
+  int32_t* pos_s = e_s + kLayoutThreads * K;
+  for (int e = tid; e < E; e += kLayoutThreads) owner_s[e] = a.owner[e];
+  if (tid < P) node_s[tid] = a.node_of[tid];
+  int32_t* totals = a.totals + (size_t)parity * E;
+  // positions survive the grid barrier in shared memory when every CTA owns
+  // exactly one chunk and both phases run in this launch (production)
+  const bool keep_pos = (phase == FS_PHASE_ALL) && nchunks <= (int)gridDim.x;
+  __syncthreads();
 
   if (phase & FS_PHASE_LOCAL) {
-    uint32_t* bits = sm;                       // [8][E]
-    uint32_t* wbase = sm + kLayoutWarps * E;   // [8][E]
+    uint32_t* bits = work;                       // [8][E]
+    uint32_t* wbase = work + kLayoutWarps * E;   // [8][E]
     long long st_dedup = 0, st_naive = 0, st_local = 0, st_node = 0;
-    const int my_node = a.node_of[s];
+    const int my_node = node_s[s];
     for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
+      const int t0 = c * kLayoutThreads;
+      const int ntok = min(kLayoutThreads, T - t0);
+      const int nel = ntok * K;
+      const size_t base_el = (size_t)t0 * K;
       for (int j = tid; j < kLayoutWarps * E; j += kLayoutThreads) bits[j] = 0u;
+      for (int j = tid; j < nel; j += kLayoutThreads) {  // coalesced index staging
+        long long e = load_idx(idx, base_el + j, a.idx64);
+        if (e < 0 || e >= E) {
+          record_error(a.status, FS_ERANGE);
+          e = 0;
+        }
+        e_s[j] = (int32_t)e;
+      }
       __syncthreads();
-      const int i = c * kLayoutThreads + tid;
-      if (i < T) {
+      if (tid < ntok) {
         uint32_t seen_node = 0u, seen_rank = 0u;
         for (int k = 0; k < K; ++k) {
-          long long e = load_idx(idx, (size_t)i * K + k, a.idx64);
-          if (e < 0 || e >= E) {
-            record_error(a.status, FS_ERANGE);
-            e = 0;
-          }
-          const int g = a.owner[e];
-          const int n = a.node_of[g];
+          const int e = e_s[tid * K + k];
+          const int g = owner_s[e];
+          const int n = node_s[g];
           const bool first = !((seen_node >> n) & 1u);
           seen_node |= 1u << n;
           seen_rank |= 1u << g;
-          if (first_mask) first_mask[(size_t)i * K + k] = first ? 1 : 0;
+          pos_s[tid * K + k] = first ? 1 : 0;  // first_mask staged here until positions overwrite it
           st_naive += (g != s);
           st_local += (g == s);
           st_node += (first && n != my_node);
           const uint32_t old = atomicOr(&bits[warp * E + e], 1u << lane);
           if (old & (1u << lane)) record_error(a.status, FS_EINVAL);  // duplicate expert in a row
         }
-        if (rank_mask) rank_mask[i] = seen_rank;
+        if (rank_mask) rank_mask[t0 + tid] = seen_rank;
         st_dedup += __popc(seen_rank & ~(1u << s));
       }
       __syncthreads();
+      if (first_mask)
+        for (int j = tid; j < nel; j += kLayoutThreads) first_mask[base_el + j] = (uint8_t)pos_s[j];
       for (int e = tid; e < E; e += kLayoutThreads) {
         uint32_t run = 0;
 #pragma unroll
@@ -101,16 +135,18 @@ __global__ void __launch_bounds__(kLayoutThreads)
           run += __popc(bits[w * E + e]);
         }
         a.chunk_cnt[(size_t)c * E + e] = (int32_t)run;
+        if (run) atomicAdd(&totals[e], (int)run);
       }
       __syncthreads();
-      if (i < T) {
+      if (tid < ntok) {
         for (int k = 0; k < K; ++k) {
-          long long e = load_idx(idx, (size_t)i * K + k, a.idx64);
-          if (e < 0 || e >= E) e = 0;
-          row_of[(size_t)i * K + k] =
-              (int32_t)(wbase[warp * E + e] + __popc(bits[warp * E + e] & lt_mask));
+          const int e = e_s[tid * K + k];
+          pos_s[tid * K + k] = (int32_t)(wbase[warp * E + e] + __popc(bits[warp * E + e] & lt_mask));
         }
       }
+      __syncthreads();
+      if (!keep_pos)
+        for (int j = tid; j < nel; j += kLayoutThreads) row_of[base_el + j] = pos_s[j];
       __syncthreads();
     }
     // block-reduce the statistics into the per-CTA partial slot
@@ -127,28 +163,21 @@ __global__ void __launch_bounds__(kLayoutThreads)
       for (int w = 0; w < kLayoutWarps; ++w) acc += red[w][tid];
       a.stat_part[blockIdx.x * 8 + tid] = acc;
     }
+    trace_stamp(a, FS_TRACE_LAYOUT_HIST);
     grid.sync();
+    trace_stamp(a, FS_TRACE_LAYOUT_GRIDSYNC);
 
-    // One CTA turns the chunk counts into per-chunk exclusive offsets and
-    // publishes this rank's per-expert totals into every peer's count matrix
-    // row [s] (the P x E count all-gather, 8 KB at P=8, E=256) — then a single
-    // release store per peer.  Only one grid-wide barrier in the kernel.
+    // One CTA publishes this rank's per-expert totals into every peer's count
+    // matrix row [s] (the P x E count all-gather, 8 KB at P=8, E=256), then
+    // one release store per peer.
     if (blockIdx.x == 0) {
+      int32_t* next_totals = a.totals + (size_t)(parity ^ 1) * E;
       for (int e = tid; e < E; e += kLayoutThreads) {
-        int run = 0;
-        for (int c0 = 0; c0 < nchunks; c0 += 8) {
-          int v[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = (c0 + j < nchunks) ? a.chunk_cnt[(size_t)(c0 + j) * E + e] : 0;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (c0 + j < nchunks) a.chunk_cnt[(size_t)(c0 + j) * E + e] = run;
-            run += v[j];
-          }
-        }
+        const int tot = ld_cg(totals + e);
+        next_totals[e] = 0;
         for (int g = 0; g < P; ++g) {
           int32_t* dst = reinterpret_cast<int32_t*>(a.peer[g] + a.off_count + (size_t)parity * a.count_stride);
-          dst[(size_t)s * E + e] = run;
+          dst[(size_t)s * E + e] = tot;
         }
       }
       if (stats && tid < 4) {
@@ -162,10 +191,10 @@ __global__ void __launch_bounds__(kLayoutThreads)
       // every CTA read the old epoch before the grid barrier: safe to bump
       if (tid == 0) *a.epoch_ptr = epoch;
       __syncthreads();
-      // release: the count rows (and the chunk offsets other CTAs of this rank
-      // read after acquiring their own flag) happen-before these stores
+      // release: the count rows happen-before these stores (bar.sync + release)
       if (tid < P)
         st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[tid] + kOffCountFlag) + s, epoch);
+      trace_stamp(a, FS_TRACE_LAYOUT_PUBLISH);
     }
   }
 
@@ -173,17 +202,19 @@ __global__ void __launch_bounds__(kLayoutThreads)
     if (tid < P)
       wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffCountFlag) + tid, epoch, a);
     __syncthreads();
-    int32_t* tot = reinterpret_cast<int32_t*>(sm);
+    trace_stamp(a, FS_TRACE_LAYOUT_WAIT);
+    int32_t* tot = reinterpret_cast<int32_t*>(work);
     int32_t* base = tot + E;
     int32_t* before = base + E;
+    int32_t* pre = before + E;
     const int32_t* cnt =
         reinterpret_cast<const int32_t*>(a.peer[s] + a.off_count + (size_t)parity * a.count_stride);
     for (int e = tid; e < E; e += kLayoutThreads) {
       int t = 0, b = 0;
       for (int q = 0; q < P; ++q) {
-        const int val = ld_relaxed_sys_s32(cnt + (size_t)q * E + e);
+        const int val = ld_cg(cnt + (size_t)q * E + e);
         t += val;
-        if (q < s) b += val;
+        b += (q < s) ? val : 0;
       }
       tot[e] = t;
       before[e] = b;
@@ -205,18 +236,25 @@ __global__ void __launch_bounds__(kLayoutThreads)
     }
     __syncthreads();
     for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
-      const int i = c * kLayoutThreads + tid;
-      if (i < T) {
-        for (int k = 0; k < K; ++k) {
-          long long e = load_idx(idx, (size_t)i * K + k, a.idx64);
-          if (e < 0 || e >= E) e = 0;
-          const size_t pos = (size_t)i * K + k;
-          const long long r =
-              (long long)row_of[pos] + base[e] + before[e] + a.chunk_cnt[(size_t)c * E + e];
-          if (r >= a.max_rows) record_error(a.status, FS_ERANGE);
-          row_of[pos] = (int32_t)r;
-        }
+      // chunk offset within (rank s, expert e): Σ of the earlier chunks' counts
+      for (int e = tid; e < E; e += kLayoutThreads) {
+        int acc = 0;
+#pragma unroll 8
+        for (int c2 = 0; c2 < c; ++c2) acc += ld_cg(a.chunk_cnt + (size_t)c2 * E + e);
+        pre[e] = base[e] + before[e] + acc;
       }
+      __syncthreads();
+      const int t0 = c * kLayoutThreads;
+      const int nel = min(kLayoutThreads, T - t0) * K;
+      const size_t base_el = (size_t)t0 * K;
+      for (int j = tid; j < nel; j += kLayoutThreads) {  // coalesced, element-wise
+        int e = keep_pos ? e_s[j] : (int)load_idx(idx, base_el + j, a.idx64);
+        if (e < 0 || e >= E) e = 0;
+        const long long r = (long long)(keep_pos ? pos_s[j] : row_of[base_el + j]) + pre[e];
+        if (r >= a.max_rows) record_error(a.status, FS_ERANGE);
+        row_of[base_el + j] = (int32_t)r;
+      }
+      __syncthreads();
     }
     if (blockIdx.x == 0) {
       const int jb = a.seg_begin[s], je = a.seg_begin[s + 1];
@@ -229,6 +267,7 @@ __global__ void __launch_bounds__(kLayoutThreads)
         if (expert_offsets) expert_offsets[je - jb] = rows_total;
         *a.num_rows = rows_total;
         if (stats) stats[FS_STAT_ROWS] = rows_total;
+        trace_stamp(a, FS_TRACE_LAYOUT_END);
         if (rows_total > a.max_rows) record_error(a.status, FS_ERANGE);
       }
     }
@@ -291,6 +330,7 @@ __global__ void __launch_bounds__(kMoveThreads)
   const int parity = (int)(epoch & 1u);
   const size_t act_off = a.off_act + (size_t)parity * a.act_stride;
   const size_t fan_off = a.off_fansrc + (size_t)parity * a.fansrc_stride;
+  trace_stamp(a, FS_TRACE_DISPATCH_BEGIN);
 
   if (phase & FS_PHASE_LOCAL) {
     const long long units = (long long)T * S;
@@ -351,11 +391,13 @@ __global__ void __launch_bounds__(kMoveThreads)
     }
   }
 
+  trace_stamp(a, FS_TRACE_DISPATCH_PUSHED);
   if ((phase & FS_PHASE_REMOTE) && P > 1) {
     if (threadIdx.x == 0)
       wait_u64_geq(reinterpret_cast<const unsigned long long*>(a.peer[s] + kOffArrive),
                    (unsigned long long)epoch * (unsigned long long)P * gridDim.x, a);
     __syncthreads();
+    trace_stamp(a, FS_TRACE_DISPATCH_ARRIVED);
     const int rows = *reinterpret_cast<volatile int*>(a.num_rows);
     const int32_t* fs = reinterpret_cast<const int32_t*>(a.peer[s] + fan_off);
     V* act = reinterpret_cast<V*>(a.peer[s] + act_off);
@@ -371,6 +413,7 @@ __global__ void __launch_bounds__(kMoveThreads)
       }
     }
   }
+  trace_stamp(a, FS_TRACE_DISPATCH_END);
 }
 
 // ===========================================================================
@@ -407,6 +450,7 @@ __global__ void __launch_bounds__(kTmaThreads)
   const int parity = (int)(epoch & 1u);
   const size_t act_off = a.off_act + (size_t)parity * a.act_stride;
   const size_t fan_off = a.off_fansrc + (size_t)parity * a.fansrc_stride;
+  trace_stamp(a, FS_TRACE_DISPATCH_BEGIN);
 
   if (phase & FS_PHASE_LOCAL) {
     if (threadIdx.x == 0) {
@@ -469,11 +513,13 @@ __global__ void __launch_bounds__(kTmaThreads)
     }
   }
 
+  trace_stamp(a, FS_TRACE_DISPATCH_PUSHED);
   if ((phase & FS_PHASE_REMOTE) && P > 1) {
     if (threadIdx.x == 0)
       wait_u64_geq(reinterpret_cast<const unsigned long long*>(a.peer[s] + kOffArrive),
                    (unsigned long long)epoch * (unsigned long long)P * gridDim.x, a);
     __syncthreads();
+    trace_stamp(a, FS_TRACE_DISPATCH_ARRIVED);
     const int rows = *reinterpret_cast<volatile int*>(a.num_rows);
     const int nv = tb / 16;
     const int32_t* fs = reinterpret_cast<const int32_t*>(a.peer[s] + fan_off);
@@ -492,6 +538,7 @@ __global__ void __launch_bounds__(kTmaThreads)
       }
     }
   }
+  trace_stamp(a, FS_TRACE_DISPATCH_END);
 }
 
 // ===========================================================================
@@ -556,16 +603,22 @@ __global__ void __launch_bounds__(kMoveThreads)
   const size_t src_off =
       src_sel == FS_SRC_ACT_OUT ? a.off_actout : a.off_act + (size_t)(epoch & 1u) * a.act_stride;
 
-  if (phase & FS_PHASE_LOCAL) {
-    if (blockIdx.x == 0 && threadIdx.x < P) {
-      __threadfence_system();
+  trace_stamp(a, FS_TRACE_COMBINE_BEGIN);
+  // "expert outputs ready" handshake: this rank's act/act_out rows were
+  // completed by earlier kernels on this stream; one release store per peer
+  // publishes them, and the pull waits for every peer's.  A single rank has
+  // nobody to wait for.
+  if ((phase & FS_PHASE_LOCAL) && P > 1) {
+    if (blockIdx.x == 0 && threadIdx.x < P)
       st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[threadIdx.x] + kOffReadyFlag) + s, epoch);
-    }
   }
   if (phase & FS_PHASE_REMOTE) {
-    if (threadIdx.x < P)
-      wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffReadyFlag) + threadIdx.x, epoch, a);
-    __syncthreads();
+    if (P > 1) {
+      if (threadIdx.x < P)
+        wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffReadyFlag) + threadIdx.x, epoch, a);
+      __syncthreads();
+    }
+    trace_stamp(a, FS_TRACE_COMBINE_READY);
     const long long units = (long long)T * S;
     for (long long u = gw; u < units; u += nw) {
       const int i = (int)(u / S);
@@ -637,6 +690,137 @@ __global__ void __launch_bounds__(kMoveThreads)
       }
     }
   }
+  trace_stamp(a, FS_TRACE_COMBINE_END);
+}
+
+// ===========================================================================
+// Combine, TMA engine
+//
+// Work item = (token i, column slice j of SB bytes).  Warp 0 resolves the
+// token's K (owner, row) pairs one item ahead and its lanes k<K each issue a
+// cp.async.bulk of row slice (owner_k, row_k, j) — local HBM or a peer over
+// NVLink — into stage q ([K][SB] bytes), all completing on full[q].
+// kCombConsumers warps then reduce Σ_k w_k·row_k in k order straight out of
+// shared memory (16 B per lane per step) and store the output slice; each
+// consumer warp arrives on empty[q] when done.  Loads in flight per SM = NS
+// stages of K·SB bytes, independent of register pressure.
+// ===========================================================================
+constexpr int kCombConsumers = 4;
+constexpr int kCombThreads = 32 * (1 + kCombConsumers);
+constexpr int kCombMaxStages = 16;
+constexpr int kCombStageTarget = 24 * 1024;  // bytes of one stage (K row slices)
+
+__host__ __device__ inline int comb_slice_bytes(int tb, int K) {
+  int sb = kCombStageTarget / K;
+  sb = sb < 512 ? 512 : sb;
+  if (sb >= tb) return tb;
+  const int S = (tb + sb - 1) / sb;
+  return (((tb + S - 1) / S) + 15) & ~15;
+}
+
+template <bool BF16, bool ACC64>
+__global__ void __launch_bounds__(kCombThreads)
+    combine_tma_kernel(FsArgs a, const void* __restrict__ idx, const int32_t* __restrict__ row_of,
+                       const void* __restrict__ topk_w, int w64, char* __restrict__ out, int src_sel,
+                       int phase, int nstages, int sb) {
+  using Acc = typename std::conditional<ACC64, double, float>::type;
+  using EL = Elem<int4, BF16>;
+  extern __shared__ __align__(128) char csm[];
+  __shared__ Acc w_s[kCombConsumers][32];
+  uint64_t* full = reinterpret_cast<uint64_t*>(csm);
+  uint64_t* empty = full + kCombMaxStages;
+  char* stages = csm + 2 * kCombMaxStages * sizeof(uint64_t);
+  const int K = a.K, T = a.T, P = a.world, s = a.rank, tb = a.tb;
+  const int S = (tb + sb - 1) / sb;
+  const int stage_bytes = K * sb;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t epoch = load_epoch(a);
+  const size_t src_off =
+      src_sel == FS_SRC_ACT_OUT ? a.off_actout : a.off_act + (size_t)(epoch & 1u) * a.act_stride;
+  trace_stamp(a, FS_TRACE_COMBINE_BEGIN);
+
+  if ((phase & FS_PHASE_LOCAL) && P > 1) {
+    if (blockIdx.x == 0 && threadIdx.x < P)
+      st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[threadIdx.x] + kOffReadyFlag) + s, epoch);
+  }
+  if (!(phase & FS_PHASE_REMOTE)) return;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < nstages; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], kCombConsumers);
+    }
+    mbar_fence_init();
+  }
+  if (P > 1 && threadIdx.x < P)
+    wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffReadyFlag) + threadIdx.x, epoch, a);
+  __syncthreads();
+  trace_stamp(a, FS_TRACE_COMBINE_READY);
+  const long long items = (long long)T * S;
+
+  if (warp == 0) {  // producer
+    int cur_tok = -1, g = 0, r = 0;
+    int n = 0;
+    for (long long u = blockIdx.x; u < items; u += gridDim.x, ++n) {
+      const int i = (int)(u / S), j = (int)(u - (long long)i * S);
+      if (i != cur_tok) {
+        cur_tok = i;
+        if (lane < K) {
+          long long e = load_idx(idx, (size_t)i * K + lane, a.idx64);
+          if (e < 0 || e >= a.E) e = 0;
+          g = a.owner[e];
+          r = row_of[(size_t)i * K + lane];
+          if (r < 0 || r >= a.max_rows) r = 0;
+        }
+      }
+      const int q = n % nstages;
+      if (n >= nstages) mbar_wait(&empty[q], ((n / nstages) & 1) ^ 1);
+      const int off = j * sb;
+      const int len = min(sb, tb - off);
+      if (lane == 0) mbar_arrive_expect_tx(&full[q], (uint32_t)(K * len));
+      __syncwarp();
+      if (lane < K)
+        bulk_load(stages + (size_t)q * stage_bytes + (size_t)lane * sb,
+                  a.peer[g] + src_off + (size_t)r * tb + off, (uint32_t)len, &full[q]);
+    }
+  } else {  // consumers
+    const int ct = threadIdx.x - 32;  // 0 .. 32*kCombConsumers-1
+    int n = 0;
+    for (long long u = blockIdx.x; u < items; u += gridDim.x, ++n) {
+      const int i = (int)(u / S), j = (int)(u - (long long)i * S);
+      const int q = n % nstages;
+      const int off = j * sb;
+      const int nv = min(sb, tb - off) / 16;
+      if (lane < K) {
+        const size_t pos = (size_t)i * K + lane;
+        w_s[warp - 1][lane] = w64 ? (Acc)reinterpret_cast<const double*>(topk_w)[pos]
+                                  : (Acc)reinterpret_cast<const float*>(topk_w)[pos];
+      }
+      __syncwarp();
+      mbar_wait(&full[q], (n / nstages) & 1);
+      const char* st = stages + (size_t)q * stage_bytes;
+      for (int v = ct; v < nv; v += 32 * kCombConsumers) {
+        Acc acc[EL::N];
+#pragma unroll
+        for (int e = 0; e < EL::N; ++e) acc[e] = (Acc)0;
+        for (int k = 0; k < K; ++k) {
+          const Acc wk = w_s[warp - 1][k];
+          const int4 x = *reinterpret_cast<const int4*>(st + (size_t)k * sb + (size_t)v * 16);
+#pragma unroll
+          for (int e = 0; e < EL::N; ++e) acc[e] = fma_acc<Acc>(wk, EL::get(x, e), acc[e]);
+        }
+        int4 o;
+#pragma unroll
+        for (int w = 0; w < EL::kWords; ++w) {
+          if constexpr (BF16) set_word(o, w, pack_out(acc[2 * w], acc[2 * w + 1]));
+          else set_word(o, w, f32_bits(acc[w]));
+        }
+        st_na(reinterpret_cast<int4*>(out + (size_t)i * tb + off) + v, o);
+      }
+      __syncwarp();  // also orders this item's w_s reads before the next item's writes
+      if (lane == 0) mbar_arrive(&empty[q]);
+    }
+  }
+  trace_stamp(a, FS_TRACE_COMBINE_END);
 }
 
 // ===========================================================================

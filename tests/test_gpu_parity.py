@@ -191,11 +191,15 @@ def test_bf16_parity_with_oracle(P, E, K, T_l, hidden, zipf):
         np.testing.assert_allclose(got, want, **BF16_TOL)
 
 
-@pytest.fixture
-def tma_dispatch(monkeypatch):
-    """Select the TMA bulk-copy dispatch engine for handles created in the test."""
-    monkeypatch.setenv("FUSCO_DISPATCH", "tma")
-    yield
+ENGINES = [("warp", "warp"), ("tma", "tma"), ("tma", "warp"), ("warp", "tma")]
+
+
+@pytest.fixture(params=ENGINES, ids=lambda e: f"dispatch-{e[0]}_combine-{e[1]}")
+def engines(request, monkeypatch):
+    """Select the dispatch / combine data movers for handles created in the test."""
+    monkeypatch.setenv("FUSCO_DISPATCH", request.param[0])
+    monkeypatch.setenv("FUSCO_COMBINE", request.param[1])
+    yield request.param
 
 
 @pytest.mark.parametrize(
@@ -205,9 +209,10 @@ def tma_dispatch(monkeypatch):
         (4, 8, 2, 1024, 4096, 0.0),
         (1, 8, 2, 2048, 4096, 0.0),
         (2, 16, 4, 333, 1024, 0.3),
+        (8, 64, 8, 64, 512, 0.0),
     ],
 )
-def test_tma_dispatch_parity_with_oracle(tma_dispatch, P, E, K, T_l, hidden, zipf):
+def test_engine_parity_with_oracle(engines, P, E, K, T_l, hidden, zipf):
     pkg, topo, pl, a, tb, payload = _cluster_case(P, E, K, T_l, hidden, "bf16", zipf, seed=P * 5 + K)
     res = _run_cluster(pkg, topo, pl, a, tb, payload, "bf16", "f64")
     layouts, row_of = _check_layout(res, a, pl, P)
@@ -216,6 +221,22 @@ def test_tma_dispatch_parity_with_oracle(tma_dispatch, P, E, K, T_l, hidden, zip
         assert np.array_equal(res["acts"][g], acts[g]), f"activation/{g}"
     for s in range(P):
         want = O.combine(acts, row_of, a.experts, a.weights, pl.owner, res["ids"][s], "bf16")
+        assert np.array_equal(res["outs"][s], want), f"output/{s}"
+    res32 = _run_cluster(pkg, topo, pl, a, tb, payload, "bf16", "f32")
+    for s in range(P):
+        want = O.decode(O.combine(acts, row_of, a.experts, a.weights, pl.owner, res["ids"][s], "bf16"), "bf16")
+        np.testing.assert_allclose(O.decode(res32["outs"][s], "bf16"), want, **BF16_TOL)
+
+
+def test_engine_parity_fp32_payload(engines):
+    """fp32 rows (the reference's own payload dtype) through both engines."""
+    pkg, topo, pl, a, tb, payload = _cluster_case(4, 32, 4, 300, 1024, "f32", 0.7, seed=9)
+    res = _run_cluster(pkg, topo, pl, a, tb, payload, "f32", "f64")
+    layouts, row_of = _check_layout(res, a, pl, 4)
+    acts = O.dispatch(payload, layouts)
+    for s in range(4):
+        assert np.array_equal(res["acts"][s], acts[s])
+        want = O.combine(acts, row_of, a.experts, a.weights, pl.owner, res["ids"][s], "f32")
         assert np.array_equal(res["outs"][s], want)
 
 

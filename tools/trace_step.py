@@ -1,0 +1,48 @@
+"""Per-phase device timeline of one shuffle step (globaltimer stamps, CTA 0).
+
+    FUSCO_TRACE=1 python tools/trace_step.py [config] [warp|tma]
+"""
+import ctypes
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+os.environ["FUSCO_TRACE"] = "1"
+cfg = sys.argv[1] if len(sys.argv) > 1 else "mixtral"
+os.environ["FUSCO_DISPATCH"] = sys.argv[2] if len(sys.argv) > 2 else "warp"
+
+import bench  # noqa: E402
+from paper_2512_22036_b200 import EPBuffer, _lib  # noqa: E402
+
+hidden, dtype, E, K, T_l, zipf, desc = bench.CONFIGS[cfg]
+a, pl = bench.routing_for(cfg, 1, 0)
+dev = torch.device("cuda", 0)
+torch.cuda.set_device(0)
+buf = EPBuffer(num_experts=E, topk=K, hidden=hidden, dtype=dtype, max_tokens=T_l, with_act_out=False)
+tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+x = torch.randn(T_l, hidden, device=dev).to(tdt)
+idx = torch.as_tensor(a.experts, device=dev)
+w = torch.as_tensor(a.weights, dtype=torch.float32, device=dev)
+names = {0: "layout.begin", 1: "layout.hist", 2: "layout.gridsync", 3: "layout.publish", 4: "layout.wait",
+         5: "layout.end", 8: "dispatch.begin", 9: "dispatch.pushed", 10: "dispatch.arrived", 11: "dispatch.end",
+         12: "combine.begin", 13: "combine.ready", 14: "combine.end"}
+lib = _lib.load()
+for it in range(30):
+    plan = buf.build_plan(idx)
+    buf.dispatch(x, plan)
+    out = buf.combine(plan, w, src="act")
+torch.cuda.synchronize()
+tr = (ctypes.c_uint64 * 16)()
+_lib.call("fs_trace", buf.r.handle, tr, _lib.stream_ptr())
+t = np.array(list(tr), dtype=np.int64)
+t0 = t[0]
+prev = t0
+for k in sorted(names):
+    if t[k]:
+        print(f"{names[k]:18s} {(t[k] - t0) / 1e3:9.2f} us  (+{(t[k] - prev) / 1e3:7.2f})")
+        prev = t[k]
+buf.close()
