@@ -198,7 +198,7 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
   *out = nullptr;
   if (world < 1 || world > FS_MAX_RANKS) return fail(FS_EINVAL, "world must be in [1, 32]");
   if (rank < 0 || rank >= world) return fail(FS_EINVAL, "rank outside [0, world)");
-  if (num_experts < 1) return fail(FS_EINVAL, "num_experts must be >= 1");
+  if (num_experts < 1 || num_experts > kMaxExperts) return fail(FS_EINVAL, "num_experts must be in [1, 1024]");
   if (topk < 1 || topk > 32 || topk > num_experts)
     return fail(FS_EINVAL, "topk must be in [1, min(32, num_experts)]");
   if (token_bytes <= 0 || token_bytes % 4)
@@ -485,12 +485,17 @@ int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes, const int32_t
                                         (cudaStream_t)stream));
     return FS_OK;
   }
+  const bool wide = h->K <= 4;  // few rows per token: pull wider slices per warp
   if (vec16) {
-    fn = bf ? (f64 ? (const void*)combine_kernel<int4, true, true> : (const void*)combine_kernel<int4, true, false>)
-            : (f64 ? (const void*)combine_kernel<int4, false, true> : (const void*)combine_kernel<int4, false, false>);
+    if (wide)
+      fn = bf ? (f64 ? (const void*)combine_kernel<int4, true, true, 8> : (const void*)combine_kernel<int4, true, false, 8>)
+              : (f64 ? (const void*)combine_kernel<int4, false, true, 8> : (const void*)combine_kernel<int4, false, false, 8>);
+    else
+      fn = bf ? (f64 ? (const void*)combine_kernel<int4, true, true, 4> : (const void*)combine_kernel<int4, true, false, 4>)
+              : (f64 ? (const void*)combine_kernel<int4, false, true, 4> : (const void*)combine_kernel<int4, false, false, 4>);
   } else {
-    fn = bf ? (f64 ? (const void*)combine_kernel<int, true, true> : (const void*)combine_kernel<int, true, false>)
-            : (f64 ? (const void*)combine_kernel<int, false, true> : (const void*)combine_kernel<int, false, false>);
+    fn = bf ? (f64 ? (const void*)combine_kernel<int, true, true, 8> : (const void*)combine_kernel<int, true, false, 8>)
+            : (f64 ? (const void*)combine_kernel<int, false, true, 8> : (const void*)combine_kernel<int, false, false, 8>);
   }
   int occ = 0;
   if (int rc = occupancy(fn, kMoveThreads, 0, &occ)) return rc;

@@ -295,6 +295,29 @@ struct MoveCfg {
   static constexpr int kSliceWords = 32 * U;
 };
 
+// Lane k < K of a warp holds (expert, row) of token i's k-th choice: two
+// independent global loads, issued one work item ahead of use; the owner is
+// looked up later in a shared-memory copy of the expert table.
+struct KMeta {
+  int e, r;
+};
+__device__ __forceinline__ KMeta load_meta(const FsArgs& a, const void* idx, const int32_t* row_of, int i,
+                                           int lane) {
+  KMeta m{0, -1};
+  if (lane < a.K) {
+    const long long e = load_idx(idx, (size_t)i * a.K + lane, a.idx64);
+    m.e = (e < 0 || e >= a.E) ? 0 : (int)e;
+    m.r = row_of[(size_t)i * a.K + lane];
+  }
+  return m;
+}
+constexpr int kMaxExperts = 1024;  // shared-memory expert table bound (checked by fs_create)
+
+__device__ __forceinline__ void load_owner_table(const FsArgs& a, int32_t* owner_sm) {
+  for (int e = threadIdx.x; e < a.E; e += blockDim.x) owner_sm[e] = a.owner[e];
+  __syncthreads();
+}
+
 template <typename V>
 __device__ __forceinline__ void warp_copy_row_cg(V* __restrict__ dst, const V* __restrict__ src, int nv,
                                                  int lane) {
@@ -333,17 +356,30 @@ __global__ void __launch_bounds__(kMoveThreads)
   trace_stamp(a, FS_TRACE_DISPATCH_BEGIN);
 
   if (phase & FS_PHASE_LOCAL) {
+    __shared__ int32_t owner_sm[kMaxExperts];
+    load_owner_table(a, owner_sm);
     const long long units = (long long)T * S;
-    for (long long u = gw; u < units; u += nw) {
+    long long u = gw;
+    KMeta nxt = u < units ? load_meta(a, idx, row_of, (int)(u / S), lane) : KMeta{0, -1};
+    for (; u < units; u += nw) {
       const int i = (int)(u / S);
       const int sl = (int)(u - (long long)i * S);
+      const KMeta cur = nxt;
+      if (u + nw < units) nxt = load_meta(a, idx, row_of, (int)((u + nw) / S), lane);
+      // payload loads first: they do not depend on the destinations
+      const int w0 = sl * SW;
+      const V* src = x + (size_t)i * nv + w0;
+      const int rem = nv - w0;
+      V v[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int w = j * 32 + lane;
+        if (w < rem) v[j] = ld_nc(src + w);
+      }
       int g = -1 - lane, r = -1;  // lanes >= K get unique negative keys
       if (lane < K) {
-        long long e = load_idx(idx, (size_t)i * K + lane, a.idx64);
-        if (e < 0 || e >= a.E) e = 0;
-        g = a.owner[e];
-        r = row_of[(size_t)i * K + lane];
-        if (r < 0 || r >= a.max_rows) r = -1;
+        g = owner_sm[cur.e];
+        r = (cur.r < 0 || cur.r >= a.max_rows) ? -1 : cur.r;
       }
       const uint32_t same = __match_any_sync(kFull, g);
       const int first_lane = __ffs(same) - 1;
@@ -353,15 +389,6 @@ __global__ void __launch_bounds__(kMoveThreads)
       if (sl == 0 && lane < K && r >= 0) {
         int32_t* fs = reinterpret_cast<int32_t*>(a.peer[g] + fan_off);
         fs[r] = direct ? r : r_first;
-      }
-      const int w0 = sl * SW;
-      const V* src = x + (size_t)i * nv + w0;
-      const int rem = nv - w0;
-      V v[U];
-#pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const int w = j * 32 + lane;
-        if (w < rem) v[j] = ld_nc(src + w);
       }
       // Rotate the destination order by token so concurrent warps of this
       // rank spread their first stores over different peers.
@@ -453,6 +480,7 @@ __global__ void __launch_bounds__(kTmaThreads)
   trace_stamp(a, FS_TRACE_DISPATCH_BEGIN);
 
   if (phase & FS_PHASE_LOCAL) {
+    __shared__ int32_t owner_tma[kMaxExperts];
     if (threadIdx.x == 0) {
       for (int q = 0; q < nslots; ++q) {
         mbar_init(&full[q], 1);
@@ -460,7 +488,7 @@ __global__ void __launch_bounds__(kTmaThreads)
       }
       mbar_fence_init();
     }
-    __syncthreads();
+    load_owner_table(a, owner_tma);
     if (warp == 0) {
       if (lane == 0) {  // producer
         int n = 0;
@@ -473,15 +501,15 @@ __global__ void __launch_bounds__(kTmaThreads)
       }
     } else if (warp == 1) {  // destinations + bulk stores
       int n = 0;
+      KMeta nxt = (int)blockIdx.x < T ? load_meta(a, idx, row_of, blockIdx.x, lane) : KMeta{0, -1};
       for (int i = blockIdx.x; i < T; i += gridDim.x, ++n) {
         const int q = n % nslots;
+        const KMeta cur = nxt;
+        if (i + (int)gridDim.x < T) nxt = load_meta(a, idx, row_of, i + gridDim.x, lane);
         int g = -1 - lane, r = -1;
         if (lane < K) {
-          long long e = load_idx(idx, (size_t)i * K + lane, a.idx64);
-          if (e < 0 || e >= a.E) e = 0;
-          g = a.owner[e];
-          r = row_of[(size_t)i * K + lane];
-          if (r < 0 || r >= a.max_rows) r = -1;
+          g = owner_tma[cur.e];
+          r = (cur.r < 0 || cur.r >= a.max_rows) ? -1 : cur.r;
         }
         const uint32_t same = __match_any_sync(kFull, g);
         const int first_lane = __ffs(same) - 1;
@@ -583,16 +611,17 @@ __device__ __forceinline__ uint32_t pack_out(double lo, double hi) {
 __device__ __forceinline__ uint32_t f32_bits(float v) { return __float_as_uint(v); }
 __device__ __forceinline__ uint32_t f32_bits(double v) { return __float_as_uint(__double2float_rn(v)); }
 
-template <typename V, bool BF16, bool ACC64>
+template <typename V, bool BF16, bool ACC64, int U>
 __global__ void __launch_bounds__(kMoveThreads)
     combine_kernel(FsArgs a, const void* __restrict__ idx, const int32_t* __restrict__ row_of,
                    const void* __restrict__ topk_w, int w64, V* __restrict__ out, int src_sel,
                    int phase) {
   using Acc = typename std::conditional<ACC64, double, float>::type;
   using EL = Elem<V, BF16>;
-  constexpr int U = sizeof(V) == 16 ? 4 : 8;  // words per lane per unit
+  // U vector words per lane per unit; KG experts' loads in flight together
+  // (U*KG = 16 words per lane: K=2 pulls wide slices, K=8 pulls 4 rows at once)
   constexpr int SW = 32 * U;
-  constexpr int KG = 4;                       // experts whose loads are in flight together
+  constexpr int KG = 16 / U < 1 ? 1 : 16 / U;
   const int K = a.K, T = a.T, P = a.world, s = a.rank;
   const int nv = a.tb / (int)sizeof(V);
   const int S = (nv + SW - 1) / SW;
@@ -619,21 +648,32 @@ __global__ void __launch_bounds__(kMoveThreads)
       __syncthreads();
     }
     trace_stamp(a, FS_TRACE_COMBINE_READY);
+    __shared__ int32_t owner_sm[kMaxExperts];
+    load_owner_table(a, owner_sm);
     const long long units = (long long)T * S;
-    for (long long u = gw; u < units; u += nw) {
+    auto load_w = [&](int i) -> Acc {
+      if (lane >= K) return (Acc)0;
+      const size_t pos = (size_t)i * K + lane;
+      return w64 ? (Acc)reinterpret_cast<const double*>(topk_w)[pos]
+                 : (Acc)reinterpret_cast<const float*>(topk_w)[pos];
+    };
+    long long u = gw;
+    KMeta nxt = u < units ? load_meta(a, idx, row_of, (int)(u / S), lane) : KMeta{0, 0};
+    Acc nxt_w = u < units ? load_w((int)(u / S)) : (Acc)0;
+    for (; u < units; u += nw) {
       const int i = (int)(u / S);
       const int sl = (int)(u - (long long)i * S);
+      const KMeta cur = nxt;
+      const Acc wk = nxt_w;
+      if (u + nw < units) {
+        const int inext = (int)((u + nw) / S);
+        nxt = load_meta(a, idx, row_of, inext, lane);
+        nxt_w = load_w(inext);
+      }
       int g = 0, r = 0;
-      Acc wk = (Acc)0;
       if (lane < K) {
-        const size_t pos = (size_t)i * K + lane;
-        long long e = load_idx(idx, pos, a.idx64);
-        if (e < 0 || e >= a.E) e = 0;
-        g = a.owner[e];
-        r = row_of[pos];
-        if (r < 0 || r >= a.max_rows) r = 0;
-        if (w64) wk = (Acc)reinterpret_cast<const double*>(topk_w)[pos];
-        else wk = (Acc)reinterpret_cast<const float*>(topk_w)[pos];
+        g = owner_sm[cur.e];
+        r = (cur.r < 0 || cur.r >= a.max_rows) ? 0 : cur.r;
       }
       const int w0 = sl * SW;
       const int rem = nv - w0;
@@ -744,6 +784,8 @@ __global__ void __launch_bounds__(kCombThreads)
       st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[threadIdx.x] + kOffReadyFlag) + s, epoch);
   }
   if (!(phase & FS_PHASE_REMOTE)) return;
+  __shared__ int32_t owner_cmb[kMaxExperts];
+  for (int e = threadIdx.x; e < a.E; e += blockDim.x) owner_cmb[e] = a.owner[e];
   if (threadIdx.x == 0) {
     for (int q = 0; q < nstages; ++q) {
       mbar_init(&full[q], 1);
@@ -760,16 +802,21 @@ __global__ void __launch_bounds__(kCombThreads)
   if (warp == 0) {  // producer
     int cur_tok = -1, g = 0, r = 0;
     int n = 0;
-    for (long long u = blockIdx.x; u < items; u += gridDim.x, ++n) {
+    long long u = blockIdx.x;
+    int nxt_tok = u < items ? (int)(u / S) : -1;
+    KMeta nxt = nxt_tok >= 0 ? load_meta(a, idx, row_of, nxt_tok, lane) : KMeta{0, 0};
+    for (; u < items; u += gridDim.x, ++n) {
       const int i = (int)(u / S), j = (int)(u - (long long)i * S);
       if (i != cur_tok) {
         cur_tok = i;
+        // nxt holds token i: consume it and prefetch the CTA's next token
+        const KMeta cur = nxt;
+        long long un = u + gridDim.x;
+        while (un < items && (int)(un / S) == i) un += gridDim.x;
+        if (un < items) nxt = load_meta(a, idx, row_of, (int)(un / S), lane);
         if (lane < K) {
-          long long e = load_idx(idx, (size_t)i * K + lane, a.idx64);
-          if (e < 0 || e >= a.E) e = 0;
-          g = a.owner[e];
-          r = row_of[(size_t)i * K + lane];
-          if (r < 0 || r >= a.max_rows) r = 0;
+          g = owner_cmb[cur.e];
+          r = (cur.r < 0 || cur.r >= a.max_rows) ? 0 : cur.r;
         }
       }
       const int q = n % nstages;
