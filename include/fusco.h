@@ -186,6 +186,14 @@ int fs_trace(fs_handle_t h, uint64_t* host_out, void* stream);
  * the link/HBM peak in-run). */
 int fs_probe_copy(int device, void* dst, const void* src, size_t bytes, int ctas, void* stream);
 
+/* All-to-all copy probe: npairs (<= 32) concurrent copies srcs[j] -> dsts[j]
+ * of `bytes` each (host arrays of device pointers, local or peer-mapped).
+ * mode 0 = warp 16-byte loads/stores, 1 = TMA bulk copies through shared
+ * memory.  Used by tools/p2p_probe.py to measure achievable NVLink push /
+ * pull bandwidth with the engines' own data movers. */
+int fs_probe_a2a(int device, void* const* dsts, const void* const* srcs, int npairs, size_t bytes,
+                 int mode, int ctas, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -61,6 +61,7 @@ struct fs_ctx {
   int move_grid;        // dispatch persistent grid (equal on all ranks)
   int dispatch_tma;     // 1: TMA bulk-copy dispatch engine (FUSCO_DISPATCH=tma)
   int tma_slots;        // smem ring slots per CTA of the TMA engine
+  int tma_lag, tma_ctas;
   size_t tma_smem;
   int combine_tma;      // 1: TMA combine engine (FUSCO_COMBINE=tma)
   int comb_sb, comb_stages, comb_grid;
@@ -277,16 +278,22 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
   {
     const char* mode = getenv("FUSCO_DISPATCH");
     h->dispatch_tma = (mode && std::string(mode) == "tma" && token_bytes % 16 == 0) ? 1 : 0;
+    const char* lag = getenv("FUSCO_TMA_LAG");
+    h->tma_lag = (lag && atoi(lag) >= 4) ? 4 : 2;
+    const char* ctas = getenv("FUSCO_TMA_CTAS");
+    h->tma_ctas = ctas ? std::max(1, std::min(8, atoi(ctas))) : 2;
     const int slot = tma_slot_bytes(token_bytes);
-    h->tma_slots = std::max(2, std::min(kTmaMaxSlots, (int)((100 * 1024 - 512) / slot)));
+    h->tma_slots = std::max(h->tma_lag + 2, std::min(kTmaMaxSlots, (int)((200 * 1024 / h->tma_ctas - 512) / slot)));
     h->tma_smem = 2 * kTmaMaxSlots * sizeof(uint64_t) + (size_t)h->tma_slots * slot;
     if (h->dispatch_tma) {
       if (h->tma_smem > 227 * 1024) return cleanup(fail(FS_EINVAL, "token too large for the TMA engine"));
-      e = cudaFuncSetAttribute(dispatch_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tma_smem);
+      const void* tfn = h->tma_lag == 4 ? (const void*)dispatch_tma_kernel<4> : (const void*)dispatch_tma_kernel<2>;
+      e = cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tma_smem);
       if (e != cudaSuccess) return cleanup(fail(FS_ECUDA, cudaGetErrorString(e)));
       int occ_t = 0;
-      if ((rc = occupancy(dispatch_tma_kernel, kTmaThreads, h->tma_smem, &occ_t))) return cleanup(rc);
-      occ_t = std::max(1, std::min(occ_t, 2));
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, tfn, kTmaThreads, h->tma_smem);
+      if (e != cudaSuccess) return cleanup(fail(FS_ECUDA, cudaGetErrorString(e)));
+      occ_t = std::max(1, std::min(occ_t, h->tma_ctas));
       h->move_grid = grid_ctas > 0 ? std::min(grid_ctas, occ_t * sms) : occ_t * sms;
     }
   }
@@ -297,7 +304,9 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
     h->combine_tma = (mode && std::string(mode) == "tma" && token_bytes % 16 == 0) ? 1 : 0;
     h->comb_sb = comb_slice_bytes(token_bytes, topk);
     const int stage = topk * h->comb_sb;
-    h->comb_stages = std::max(2, std::min(kCombMaxStages, (100 * 1024) / stage));
+    const char* cctas = getenv("FUSCO_TMA_CTAS");
+    const int comb_ctas = cctas ? std::max(1, std::min(8, atoi(cctas))) : 2;
+    h->comb_stages = std::max(2, std::min(kCombMaxStages, (200 * 1024 / comb_ctas) / stage));
     h->comb_smem = 2 * kCombMaxStages * sizeof(uint64_t) + (size_t)h->comb_stages * stage;
     h->comb_grid = 0;
     if (h->combine_tma) {
@@ -313,7 +322,7 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
         if (e != cudaSuccess) return cleanup(fail(FS_ECUDA, cudaGetErrorString(e)));
         occ_c = std::min(occ_c, o2);
       }
-      occ_c = std::max(1, std::min(occ_c, 2));
+      occ_c = std::max(1, std::min(occ_c, comb_ctas));
       h->comb_grid = grid_ctas > 0 ? std::min(grid_ctas, occ_c * sms) : occ_c * sms;
     }
   }
@@ -440,7 +449,8 @@ int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_byte
     if (!vec16) return fail(FS_EINVAL, "TMA dispatch needs 16-byte aligned rows");
     int nslots = h->tma_slots;
     void* targs[] = {&a, (void*)&x, (void*)&topk_idx, (void*)&row_of, &phase, &nslots};
-    FS_CUDA(cudaLaunchCooperativeKernel((const void*)dispatch_tma_kernel, dim3(h->move_grid), dim3(kTmaThreads),
+    const void* tfn = h->tma_lag == 4 ? (const void*)dispatch_tma_kernel<4> : (const void*)dispatch_tma_kernel<2>;
+    FS_CUDA(cudaLaunchCooperativeKernel(tfn, dim3(h->move_grid), dim3(kTmaThreads),
                                         targs, h->tma_smem, (cudaStream_t)stream));
     return FS_OK;
   }
@@ -485,17 +495,17 @@ int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes, const int32_t
                                         (cudaStream_t)stream));
     return FS_OK;
   }
-  const bool wide = h->K <= 4;  // few rows per token: pull wider slices per warp
+  // rows in flight per unit: min(K, 4) (no registers reserved for loads that never issue)
   if (vec16) {
-    if (wide)
-      fn = bf ? (f64 ? (const void*)combine_kernel<int4, true, true, 8> : (const void*)combine_kernel<int4, true, false, 8>)
-              : (f64 ? (const void*)combine_kernel<int4, false, true, 8> : (const void*)combine_kernel<int4, false, false, 8>);
+    if (h->K <= 2)
+      fn = bf ? (f64 ? (const void*)combine_kernel<int4, true, true, 4, 2> : (const void*)combine_kernel<int4, true, false, 4, 2>)
+              : (f64 ? (const void*)combine_kernel<int4, false, true, 4, 2> : (const void*)combine_kernel<int4, false, false, 4, 2>);
     else
-      fn = bf ? (f64 ? (const void*)combine_kernel<int4, true, true, 4> : (const void*)combine_kernel<int4, true, false, 4>)
-              : (f64 ? (const void*)combine_kernel<int4, false, true, 4> : (const void*)combine_kernel<int4, false, false, 4>);
+      fn = bf ? (f64 ? (const void*)combine_kernel<int4, true, true, 4, 4> : (const void*)combine_kernel<int4, true, false, 4, 4>)
+              : (f64 ? (const void*)combine_kernel<int4, false, true, 4, 4> : (const void*)combine_kernel<int4, false, false, 4, 4>);
   } else {
-    fn = bf ? (f64 ? (const void*)combine_kernel<int, true, true, 8> : (const void*)combine_kernel<int, true, false, 8>)
-            : (f64 ? (const void*)combine_kernel<int, false, true, 8> : (const void*)combine_kernel<int, false, false, 8>);
+    fn = bf ? (f64 ? (const void*)combine_kernel<int, true, true, 8, 4> : (const void*)combine_kernel<int, true, false, 8, 4>)
+            : (f64 ? (const void*)combine_kernel<int, false, true, 8, 4> : (const void*)combine_kernel<int, false, false, 8, 4>);
   }
   int occ = 0;
   if (int rc = occupancy(fn, kMoveThreads, 0, &occ)) return rc;
@@ -526,6 +536,30 @@ int fs_trace(fs_handle_t h, uint64_t* host_out, void* stream) {
   FS_CUDA(cudaSetDevice(h->device));
   FS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   FS_CUDA(cudaMemcpy(host_out, h->trace_d, FS_NTRACE * 8, cudaMemcpyDeviceToHost));
+  return FS_OK;
+}
+
+int fs_probe_a2a(int device, void* const* dsts, const void* const* srcs, int npairs, size_t bytes, int mode,
+                 int ctas, void* stream) {
+  if (!dsts || !srcs || npairs < 1 || npairs > FS_MAX_RANKS || bytes % 16 || ctas <= 0 || (mode != 0 && mode != 1))
+    return fail(FS_EINVAL, "fs_probe_a2a: bad arguments");
+  FS_CUDA(cudaSetDevice(device));
+  ProbePairs pp;
+  memset(&pp, 0, sizeof(pp));
+  for (int j = 0; j < npairs; ++j) {
+    if (!aligned(dsts[j], 16) || !aligned(srcs[j], 16)) return fail(FS_EINVAL, "fs_probe_a2a: 16-byte alignment");
+    pp.dst[j] = (char*)dsts[j];
+    pp.src[j] = (const char*)srcs[j];
+  }
+  if (mode == 0) {
+    probe_a2a_warp_kernel<<<ctas, kMoveThreads, 0, (cudaStream_t)stream>>>(pp, npairs, bytes);
+  } else {
+    const int nslots = 6;
+    const size_t smem = 32 * sizeof(uint64_t) + (size_t)nslots * kProbeChunk;
+    FS_CUDA(cudaFuncSetAttribute(probe_a2a_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    probe_a2a_tma_kernel<<<ctas, 64, smem, (cudaStream_t)stream>>>(pp, npairs, bytes, nslots);
+  }
+  FS_CUDA(cudaGetLastError());
   return FS_OK;
 }
 

@@ -459,10 +459,10 @@ __global__ void __launch_bounds__(kMoveThreads)
 // ===========================================================================
 constexpr int kTmaThreads = 128;
 constexpr int kTmaMaxSlots = 32;
-constexpr int kTmaLag = 2;  // bulk groups allowed to still be reading smem
 
 __host__ __device__ inline int tma_slot_bytes(int tb) { return (tb + 127) & ~127; }
 
+template <int LAG>
 __global__ void __launch_bounds__(kTmaThreads)
     dispatch_tma_kernel(FsArgs a, const char* __restrict__ x, const void* __restrict__ idx,
                         const int32_t* __restrict__ row_of, int phase, int nslots) {
@@ -526,9 +526,9 @@ __global__ void __launch_bounds__(kTmaThreads)
         if (direct)
           bulk_store(a.peer[g] + act_off + (size_t)r * tb, ring + (size_t)q * slot_bytes, (uint32_t)tb);
         bulk_commit();
-        bulk_wait_read<kTmaLag>();
+        bulk_wait_read<LAG>();
         __syncwarp();
-        if (lane == 0 && n >= kTmaLag) mbar_arrive(&empty[(n - kTmaLag) % nslots]);
+        if (lane == 0 && n >= LAG) mbar_arrive(&empty[(n - LAG) % nslots]);
       }
       bulk_wait<0>();
       fence_proxy_async_global();
@@ -611,17 +611,16 @@ __device__ __forceinline__ uint32_t pack_out(double lo, double hi) {
 __device__ __forceinline__ uint32_t f32_bits(float v) { return __float_as_uint(v); }
 __device__ __forceinline__ uint32_t f32_bits(double v) { return __float_as_uint(__double2float_rn(v)); }
 
-template <typename V, bool BF16, bool ACC64, int U>
+template <typename V, bool BF16, bool ACC64, int U, int KG>
 __global__ void __launch_bounds__(kMoveThreads)
     combine_kernel(FsArgs a, const void* __restrict__ idx, const int32_t* __restrict__ row_of,
                    const void* __restrict__ topk_w, int w64, V* __restrict__ out, int src_sel,
                    int phase) {
   using Acc = typename std::conditional<ACC64, double, float>::type;
   using EL = Elem<V, BF16>;
-  // U vector words per lane per unit; KG experts' loads in flight together
-  // (U*KG = 16 words per lane: K=2 pulls wide slices, K=8 pulls 4 rows at once)
+  // U vector words per lane per unit; KG experts' rows in flight together
+  // (KG = min(K, 4) so no registers are reserved for loads that never issue)
   constexpr int SW = 32 * U;
-  constexpr int KG = 16 / U < 1 ? 1 : 16 / U;
   const int K = a.K, T = a.T, P = a.world, s = a.rank;
   const int nv = a.tb / (int)sizeof(V);
   const int S = (nv + SW - 1) / SW;
@@ -832,16 +831,20 @@ __global__ void __launch_bounds__(kCombThreads)
   } else {  // consumers
     const int ct = threadIdx.x - 32;  // 0 .. 32*kCombConsumers-1
     int n = 0;
+    auto load_w = [&](long long uu) -> Acc {
+      if (lane >= K || uu >= items) return (Acc)0;
+      const size_t pos = (size_t)(uu / S) * K + lane;
+      return w64 ? (Acc)reinterpret_cast<const double*>(topk_w)[pos]
+                 : (Acc)reinterpret_cast<const float*>(topk_w)[pos];
+    };
+    Acc w_next = load_w(blockIdx.x);
     for (long long u = blockIdx.x; u < items; u += gridDim.x, ++n) {
       const int i = (int)(u / S), j = (int)(u - (long long)i * S);
       const int q = n % nstages;
       const int off = j * sb;
       const int nv = min(sb, tb - off) / 16;
-      if (lane < K) {
-        const size_t pos = (size_t)i * K + lane;
-        w_s[warp - 1][lane] = w64 ? (Acc)reinterpret_cast<const double*>(topk_w)[pos]
-                                  : (Acc)reinterpret_cast<const float*>(topk_w)[pos];
-      }
+      if (lane < K) w_s[warp - 1][lane] = w_next;
+      w_next = load_w(u + gridDim.x);  // in flight while this item is reduced
       __syncwarp();
       mbar_wait(&full[q], (n / nstages) & 1);
       const char* st = stages + (size_t)q * stage_bytes;
@@ -892,6 +895,81 @@ __global__ void __launch_bounds__(kMoveThreads)
       if (w < n16) st_na(dst + w, v[j]);
     }
   }
+}
+
+// ===========================================================================
+// All-to-all copy probe: pairs j = 0..n-1 copy src[j] -> dst[j] concurrently
+// (chunks interleaved over CTAs so every pair progresses at once).  With
+// src local / dst on peers it measures NVLink push bandwidth, with src on
+// peers / dst local the pull bandwidth — with the engines' own movers
+// (mode 0: warp 16 B loads/stores, mode 1: TMA bulk via a smem ring).
+// ===========================================================================
+struct ProbePairs {
+  const char* src[FS_MAX_RANKS];
+  char* dst[FS_MAX_RANKS];
+};
+constexpr int kProbeChunk = 16384;
+
+__global__ void __launch_bounds__(kMoveThreads) probe_a2a_warp_kernel(ProbePairs pp, int npairs, size_t bytes) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  const long long chunks = (long long)((bytes + kProbeChunk - 1) / kProbeChunk) * npairs;
+  for (long long c = gw; c < chunks; c += nw) {
+    const int j = (int)(c % npairs);
+    const size_t off = (size_t)(c / npairs) * kProbeChunk;
+    const int n16 = (int)(min((size_t)kProbeChunk, bytes - off) / 16);
+    const int4* s = reinterpret_cast<const int4*>(pp.src[j] + off);
+    int4* d = reinterpret_cast<int4*>(pp.dst[j] + off);
+    for (int w0 = 0; w0 < n16; w0 += 32 * 8) {
+      int4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (w0 + u * 32 + lane < n16) v[u] = ld_nc(s + w0 + u * 32 + lane);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (w0 + u * 32 + lane < n16) st_na(d + w0 + u * 32 + lane, v[u]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(64) probe_a2a_tma_kernel(ProbePairs pp, int npairs, size_t bytes, int nslots) {
+  extern __shared__ __align__(128) char psm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(psm);
+  char* ring = psm + 32 * sizeof(uint64_t);
+  if (threadIdx.x != 0) return;  // one thread drives loads and stores
+  for (int q = 0; q < nslots; ++q) mbar_init(&full[q], 1);
+  mbar_fence_init();
+  const long long chunks = (long long)((bytes + kProbeChunk - 1) / kProbeChunk) * npairs;
+  long long n = 0;
+  // prologue: fill the ring
+  long long c_load = blockIdx.x;
+  for (int q = 0; q < nslots && c_load < chunks; ++q, c_load += gridDim.x) {
+    const int j = (int)(c_load % npairs);
+    const size_t off = (size_t)(c_load / npairs) * kProbeChunk;
+    const uint32_t len = (uint32_t)min((size_t)kProbeChunk, bytes - off);
+    mbar_arrive_expect_tx(&full[q], len);
+    bulk_load(ring + (size_t)q * kProbeChunk, pp.src[j] + off, len, &full[q]);
+  }
+  for (long long c = blockIdx.x; c < chunks; c += gridDim.x, ++n) {
+    const int q = (int)(n % nslots);
+    mbar_wait(&full[q], (uint32_t)((n / nslots) & 1));
+    const int j = (int)(c % npairs);
+    const size_t off = (size_t)(c / npairs) * kProbeChunk;
+    const uint32_t len = (uint32_t)min((size_t)kProbeChunk, bytes - off);
+    bulk_store(pp.dst[j] + off, ring + (size_t)q * kProbeChunk, len);
+    bulk_commit();
+    bulk_wait_read<0>();
+    if (c_load < chunks) {  // refill this slot
+      const int j2 = (int)(c_load % npairs);
+      const size_t off2 = (size_t)(c_load / npairs) * kProbeChunk;
+      const uint32_t len2 = (uint32_t)min((size_t)kProbeChunk, bytes - off2);
+      mbar_arrive_expect_tx(&full[q], len2);
+      bulk_load(ring + (size_t)q * kProbeChunk, pp.src[j2] + off2, len2, &full[q]);
+      c_load += gridDim.x;
+    }
+  }
+  bulk_wait<0>();
 }
 
 }  // namespace fusco
