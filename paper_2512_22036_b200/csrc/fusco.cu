@@ -456,7 +456,7 @@ int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_byte
   }
   void* args[] = {&a, (void*)&x, (void*)&topk_idx, (void*)&row_of, &phase};
   const void* fn = vec16 ? (const void*)dispatch_kernel<int4> : (const void*)dispatch_kernel<int>;
-  // fixed grid: receivers expect epoch * world * move_grid arrival signals
+  // fixed grid per handle: the done counter of a rank reaches epoch * move_grid
   FS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(h->move_grid), dim3(kMoveThreads), args, 0,
                                       (cudaStream_t)stream));
   return FS_OK;

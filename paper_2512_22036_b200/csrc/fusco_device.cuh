@@ -24,7 +24,8 @@ constexpr uint32_t kFull = 0xffffffffu;
 constexpr size_t kSigBytes = 4096;
 constexpr size_t kOffCountFlag = 0;    // u32[FS_MAX_RANKS]: layout counts published
 constexpr size_t kOffReadyFlag = 256;  // u32[FS_MAX_RANKS]: expert outputs ready
-constexpr size_t kOffArrive = 512;     // u64: dispatch CTAs that finished pushing here
+constexpr size_t kOffArrive = 512;     // u32[FS_MAX_RANKS]: source s finished pushing here (epoch)
+constexpr size_t kOffDone = 1024;      // u64: this rank's dispatch CTAs done pushing (epoch * grid)
 
 struct FsArgs {
   int rank, world, E, K, tb, T;
@@ -84,6 +85,12 @@ __device__ __forceinline__ int ld_relaxed_sys_s32(const int32_t* p) {
 __device__ __forceinline__ void st_release_sys_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long atom_add_acq_rel_gpu_u64(unsigned long long* p,
+                                                                        unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void red_release_sys_add_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -111,6 +118,21 @@ __device__ __forceinline__ bool wait_u64_geq(const unsigned long long* p, unsign
   return true;
 }
 
+// End of a rank's push phase: every CTA counts itself done on a local
+// counter (acq_rel, cumulative over the CTA's stores through bar.sync); the
+// last CTA of the epoch then releases one flag per peer (value = epoch).
+// One NVLink signal per (source, destination) instead of one per CTA.
+__device__ __forceinline__ void signal_pushed(const FsArgs& a, uint32_t epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long* done = reinterpret_cast<unsigned long long*>(a.peer[a.rank] + kOffDone);
+    const unsigned long long prev = atom_add_acq_rel_gpu_u64(done, 1ull);
+    if (prev + 1 == (unsigned long long)epoch * gridDim.x) {
+      for (int g = 0; g < a.world; ++g)
+        st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[g] + kOffArrive) + a.rank, epoch);
+    }
+  }
+}
 // ---- 16-byte / 4-byte vector moves ----------------------------------------
 // Read-only inputs (x, peers' finished act/act_out): non-coherent path, no L1
 // allocation (streaming).  Data written by peers inside the same kernel

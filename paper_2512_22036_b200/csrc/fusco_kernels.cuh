@@ -409,20 +409,13 @@ __global__ void __launch_bounds__(kMoveThreads)
         }
       }
     }
-    if (P > 1) {
-      // release (cumulative over the CTA's stores via bar.sync) per peer
-      __syncthreads();
-      if (threadIdx.x < P)
-        red_release_sys_add_u64(
-            reinterpret_cast<unsigned long long*>(a.peer[threadIdx.x] + kOffArrive), 1ull);
-    }
+    if (P > 1) signal_pushed(a, epoch);
   }
 
   trace_stamp(a, FS_TRACE_DISPATCH_PUSHED);
   if ((phase & FS_PHASE_REMOTE) && P > 1) {
-    if (threadIdx.x == 0)
-      wait_u64_geq(reinterpret_cast<const unsigned long long*>(a.peer[s] + kOffArrive),
-                   (unsigned long long)epoch * (unsigned long long)P * gridDim.x, a);
+    if (threadIdx.x < P)
+      wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffArrive) + threadIdx.x, epoch, a);
     __syncthreads();
     trace_stamp(a, FS_TRACE_DISPATCH_ARRIVED);
     const int rows = *reinterpret_cast<volatile int*>(a.num_rows);
@@ -533,19 +526,13 @@ __global__ void __launch_bounds__(kTmaThreads)
       bulk_wait<0>();
       fence_proxy_async_global();
     }
-    if (P > 1) {
-      __syncthreads();
-      if (threadIdx.x < P)
-        red_release_sys_add_u64(
-            reinterpret_cast<unsigned long long*>(a.peer[threadIdx.x] + kOffArrive), 1ull);
-    }
+    if (P > 1) signal_pushed(a, epoch);
   }
 
   trace_stamp(a, FS_TRACE_DISPATCH_PUSHED);
   if ((phase & FS_PHASE_REMOTE) && P > 1) {
-    if (threadIdx.x == 0)
-      wait_u64_geq(reinterpret_cast<const unsigned long long*>(a.peer[s] + kOffArrive),
-                   (unsigned long long)epoch * (unsigned long long)P * gridDim.x, a);
+    if (threadIdx.x < P)
+      wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffArrive) + threadIdx.x, epoch, a);
     __syncthreads();
     trace_stamp(a, FS_TRACE_DISPATCH_ARRIVED);
     const int rows = *reinterpret_cast<volatile int*>(a.num_rows);

@@ -1,6 +1,7 @@
 """Per-phase device timeline of one shuffle step (globaltimer stamps, CTA 0).
 
-    FUSCO_TRACE=1 python tools/trace_step.py [config] [warp|tma]
+    FUSCO_TRACE=1 python tools/trace_step.py [config] [warp|tma] [warp|tma]
+    torchrun --nproc-per-node N tools/trace_step.py ...   (one timeline per rank)
 """
 import ctypes
 import os
@@ -14,19 +15,28 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 os.environ["FUSCO_TRACE"] = "1"
 cfg = sys.argv[1] if len(sys.argv) > 1 else "mixtral"
 os.environ["FUSCO_DISPATCH"] = sys.argv[2] if len(sys.argv) > 2 else "warp"
+os.environ["FUSCO_COMBINE"] = sys.argv[3] if len(sys.argv) > 3 else os.environ["FUSCO_DISPATCH"]
 
 import bench  # noqa: E402
 from paper_2512_22036_b200 import EPBuffer, _lib  # noqa: E402
 
+import torch.distributed as dist  # noqa: E402
+
 hidden, dtype, E, K, T_l, zipf, desc = bench.CONFIGS[cfg]
-a, pl = bench.routing_for(cfg, 1, 0)
-dev = torch.device("cuda", 0)
-torch.cuda.set_device(0)
+world = int(os.environ.get("WORLD_SIZE", 1))
+local = int(os.environ.get("LOCAL_RANK", 0))
+dev = torch.device("cuda", local)
+torch.cuda.set_device(local)
+if world > 1:
+    dist.init_process_group("nccl", device_id=dev)
+rank = dist.get_rank() if world > 1 else 0
+a, pl = bench.routing_for(cfg, world, 0)
+sel = np.flatnonzero(a.source == rank)
 buf = EPBuffer(num_experts=E, topk=K, hidden=hidden, dtype=dtype, max_tokens=T_l, with_act_out=False)
 tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
 x = torch.randn(T_l, hidden, device=dev).to(tdt)
-idx = torch.as_tensor(a.experts, device=dev)
-w = torch.as_tensor(a.weights, dtype=torch.float32, device=dev)
+idx = torch.as_tensor(a.experts[sel], device=dev)
+w = torch.as_tensor(a.weights[sel], dtype=torch.float32, device=dev)
 names = {0: "layout.begin", 1: "layout.hist", 2: "layout.gridsync", 3: "layout.publish", 4: "layout.wait",
          5: "layout.end", 8: "dispatch.begin", 9: "dispatch.pushed", 10: "dispatch.arrived", 11: "dispatch.end",
          12: "combine.begin", 13: "combine.ready", 14: "combine.end"}
@@ -39,10 +49,25 @@ torch.cuda.synchronize()
 tr = (ctypes.c_uint64 * 16)()
 _lib.call("fs_trace", buf.r.handle, tr, _lib.stream_ptr())
 t = np.array(list(tr), dtype=np.int64)
+lines = [f"[rank {rank}] {cfg} world={world}"]
 t0 = t[0]
+if world > 1:  # common time origin: min layout.begin over ranks (globaltimer is per GPU; close enough)
+    tt = torch.tensor([t0], dtype=torch.int64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MIN)
+    t0 = int(tt.item())
 prev = t0
 for k in sorted(names):
     if t[k]:
-        print(f"{names[k]:18s} {(t[k] - t0) / 1e3:9.2f} us  (+{(t[k] - prev) / 1e3:7.2f})")
+        lines.append(f"  {names[k]:18s} {(t[k] - t0) / 1e3:9.2f} us  (+{(t[k] - prev) / 1e3:7.2f})")
         prev = t[k]
-buf.close()
+if world > 1:
+    out = [None] * world
+    dist.all_gather_object(out, "\n".join(lines))
+    if rank == 0:
+        print("\n".join(out), flush=True)
+    dist.barrier()
+    buf.close()
+    dist.destroy_process_group()
+else:
+    print("\n".join(lines))
+    buf.close()
