@@ -335,7 +335,7 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
       (e = dalloc((void**)&h->seg_d, (world + 1) * 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->chunk_cnt_d, (size_t)max_chunks * num_experts * 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->totals_d, (size_t)2 * num_experts * 4)) != cudaSuccess ||
-      (e = dalloc((void**)&h->stat_part_d, (size_t)h->layout_grid_max * 8 * 8)) != cudaSuccess ||
+      (e = dalloc((void**)&h->stat_part_d, (size_t)2 * 8 * 8)) != cudaSuccess ||
       (e = dalloc((void**)&h->status_d, 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->num_rows_d, 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->epoch_d, 4)) != cudaSuccess)
@@ -348,6 +348,7 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
       (e = cudaMemset(h->num_rows_d, 0, 4)) != cudaSuccess ||
       (e = cudaMemset(h->epoch_d, 0, 4)) != cudaSuccess ||
       (e = cudaMemset(h->totals_d, 0, (size_t)2 * num_experts * 4)) != cudaSuccess ||
+      (e = cudaMemset(h->stat_part_d, 0, (size_t)2 * 8 * 8)) != cudaSuccess ||
       (e = cudaDeviceSynchronize()) != cudaSuccess)
     return cleanup(fail(FS_ECUDA, std::string("fs_create init: ") + cudaGetErrorString(e)));
   {

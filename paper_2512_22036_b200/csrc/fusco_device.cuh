@@ -45,7 +45,7 @@ struct FsArgs {
   size_t count_stride, fansrc_stride, act_stride;  // bytes per parity copy
   int32_t* chunk_cnt;        // [chunks][E] scratch (per handle)
   int32_t* totals;           // [2][E] per-parity per-expert atomic totals (per handle)
-  long long* stat_part;      // [layout grid][8] scratch
+  long long* stat_part;      // [2][8] per-parity atomic statistics accumulators
   int* status;               // first error code, FS_OK when clean
   int* num_rows;             // rows of the own activation buffer this epoch
   unsigned long long timeout_ns;

@@ -77,34 +77,47 @@ __global__ void __launch_bounds__(kLayoutThreads)
   const size_t work_words = (size_t)(2 * kLayoutWarps * E > 4 * E ? 2 * kLayoutWarps * E : 4 * E);
   int32_t* e_s = reinterpret_cast<int32_t*>(work + work_words);
   int32_t* pos_s = e_s + kLayoutThreads * K;
-  for (int e = tid; e < E; e += kLayoutThreads) owner_s[e] = a.owner[e];
-  if (tid < P) node_s[tid] = a.node_of[tid];
   int32_t* totals = a.totals + (size_t)parity * E;
+  long long* stat_acc = a.stat_part + parity * 8;  // [2][8] per-parity atomic accumulators
   // positions survive the grid barrier in shared memory when every CTA owns
   // exactly one chunk and both phases run in this launch (production)
   const bool keep_pos = (phase == FS_PHASE_ALL) && nchunks <= (int)gridDim.x;
-  __syncthreads();
+
+  // stage the expert table and this CTA's first chunk of indices together
+  // (one memory round trip instead of two)
+  for (int e = tid; e < E; e += kLayoutThreads) owner_s[e] = a.owner[e];
+  if (tid < P) node_s[tid] = a.node_of[tid];
+  auto stage_chunk = [&](int c) {
+    const int t0 = c * kLayoutThreads;
+    const int nel = min(kLayoutThreads, T - t0) * K;
+    const size_t base_el = (size_t)t0 * K;
+    for (int j = tid; j < nel; j += kLayoutThreads) {
+      long long e = load_idx(idx, base_el + j, a.idx64);
+      if (e < 0 || e >= E) {
+        record_error(a.status, FS_ERANGE);
+        e = 0;
+      }
+      e_s[j] = (int32_t)e;
+    }
+  };
+  if ((phase & FS_PHASE_LOCAL) && (int)blockIdx.x < nchunks) stage_chunk(blockIdx.x);
 
   if (phase & FS_PHASE_LOCAL) {
     uint32_t* bits = work;                       // [8][E]
     uint32_t* wbase = work + kLayoutWarps * E;   // [8][E]
     long long st_dedup = 0, st_naive = 0, st_local = 0, st_node = 0;
-    const int my_node = node_s[s];
     for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
       const int t0 = c * kLayoutThreads;
       const int ntok = min(kLayoutThreads, T - t0);
       const int nel = ntok * K;
       const size_t base_el = (size_t)t0 * K;
-      for (int j = tid; j < kLayoutWarps * E; j += kLayoutThreads) bits[j] = 0u;
-      for (int j = tid; j < nel; j += kLayoutThreads) {  // coalesced index staging
-        long long e = load_idx(idx, base_el + j, a.idx64);
-        if (e < 0 || e >= E) {
-          record_error(a.status, FS_ERANGE);
-          e = 0;
-        }
-        e_s[j] = (int32_t)e;
+      if (c != (int)blockIdx.x) {
+        __syncthreads();
+        stage_chunk(c);
       }
+      for (int j = tid; j < kLayoutWarps * E; j += kLayoutThreads) bits[j] = 0u;
       __syncthreads();
+      const int my_node = node_s[s];
       if (tid < ntok) {
         uint32_t seen_node = 0u, seen_rank = 0u;
         for (int k = 0; k < K; ++k) {
@@ -147,9 +160,8 @@ __global__ void __launch_bounds__(kLayoutThreads)
       __syncthreads();
       if (!keep_pos)
         for (int j = tid; j < nel; j += kLayoutThreads) row_of[base_el + j] = pos_s[j];
-      __syncthreads();
     }
-    // block-reduce the statistics into the per-CTA partial slot
+    // statistics: block reduce, then one commutative atomic per counter
     long long v[4] = {st_dedup, st_naive, st_local, st_node};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -161,7 +173,7 @@ __global__ void __launch_bounds__(kLayoutThreads)
     if (tid < 4) {
       long long acc = 0;
       for (int w = 0; w < kLayoutWarps; ++w) acc += red[w][tid];
-      a.stat_part[blockIdx.x * 8 + tid] = acc;
+      if (acc) atomicAdd(reinterpret_cast<unsigned long long*>(stat_acc + tid), (unsigned long long)acc);
     }
     trace_stamp(a, FS_TRACE_LAYOUT_HIST);
     grid.sync();
@@ -169,55 +181,75 @@ __global__ void __launch_bounds__(kLayoutThreads)
 
     // One CTA publishes this rank's per-expert totals into every peer's count
     // matrix row [s] (the P x E count all-gather, 8 KB at P=8, E=256), then
-    // one release store per peer.
+    // one release store per peer.  A single rank needs no publication.
     if (blockIdx.x == 0) {
       int32_t* next_totals = a.totals + (size_t)(parity ^ 1) * E;
-      for (int e = tid; e < E; e += kLayoutThreads) {
-        const int tot = ld_cg(totals + e);
-        next_totals[e] = 0;
-        for (int g = 0; g < P; ++g) {
-          int32_t* dst = reinterpret_cast<int32_t*>(a.peer[g] + a.off_count + (size_t)parity * a.count_stride);
-          dst[(size_t)s * E + e] = tot;
+      long long* next_stats = a.stat_part + (parity ^ 1) * 8;
+      if (P > 1) {
+        for (int e = tid; e < E; e += kLayoutThreads) {
+          const int tot = ld_cg(totals + e);
+          for (int g = 0; g < P; ++g) {
+            int32_t* dst = reinterpret_cast<int32_t*>(a.peer[g] + a.off_count + (size_t)parity * a.count_stride);
+            dst[(size_t)s * E + e] = tot;
+          }
         }
       }
+      for (int e = tid; e < E; e += kLayoutThreads) next_totals[e] = 0;
       if (stats && tid < 4) {
-        long long acc = 0;
-        for (int b = 0; b < (int)gridDim.x; ++b) acc += a.stat_part[b * 8 + tid];
-        const int slot[4] = {FS_STAT_DEDUP_SEND, FS_STAT_NAIVE_SEND, FS_STAT_LOCAL_ROWS,
-                             FS_STAT_NODE_DEDUP};
-        stats[slot[tid]] = acc;
+        const int slot[4] = {FS_STAT_DEDUP_SEND, FS_STAT_NAIVE_SEND, FS_STAT_LOCAL_ROWS, FS_STAT_NODE_DEDUP};
+        stats[slot[tid]] = *reinterpret_cast<volatile long long*>(stat_acc + tid);
       }
       if (stats && tid >= 5 && tid < FS_NSTATS) stats[tid] = 0;
+      if (tid < 8) next_stats[tid] = 0;
       // every CTA read the old epoch before the grid barrier: safe to bump
       if (tid == 0) *a.epoch_ptr = epoch;
-      __syncthreads();
-      // release: the count rows happen-before these stores (bar.sync + release)
-      if (tid < P)
-        st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[tid] + kOffCountFlag) + s, epoch);
+      if (P > 1) {
+        __syncthreads();
+        // release: the count rows happen-before these stores (bar.sync + release)
+        if (tid < P)
+          st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[tid] + kOffCountFlag) + s, epoch);
+      }
       trace_stamp(a, FS_TRACE_LAYOUT_PUBLISH);
     }
   }
 
   if (phase & FS_PHASE_REMOTE) {
-    if (tid < P)
-      wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffCountFlag) + tid, epoch, a);
-    __syncthreads();
-    trace_stamp(a, FS_TRACE_LAYOUT_WAIT);
     int32_t* tot = reinterpret_cast<int32_t*>(work);
     int32_t* base = tot + E;
     int32_t* before = base + E;
     int32_t* pre = before + E;
-    const int32_t* cnt =
-        reinterpret_cast<const int32_t*>(a.peer[s] + a.off_count + (size_t)parity * a.count_stride);
-    for (int e = tid; e < E; e += kLayoutThreads) {
-      int t = 0, b = 0;
-      for (int q = 0; q < P; ++q) {
-        const int val = ld_cg(cnt + (size_t)q * E + e);
-        t += val;
-        b += (q < s) ? val : 0;
+    // this CTA's chunk offsets Σ_{c'<c} cnt[c'][e] — issued before the peer
+    // wait so their latency overlaps it (only the CTA's first chunk here)
+    const int c_first = blockIdx.x;
+    if (c_first < nchunks)
+      for (int e = tid; e < E; e += kLayoutThreads) {
+        int acc = 0;
+#pragma unroll 8
+        for (int c2 = 0; c2 < c_first; ++c2) acc += ld_cg(a.chunk_cnt + (size_t)c2 * E + e);
+        pre[e] = acc;
       }
-      tot[e] = t;
-      before[e] = b;
+    if (P > 1) {
+      if (tid < P)
+        wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffCountFlag) + tid, epoch, a);
+      __syncthreads();
+      trace_stamp(a, FS_TRACE_LAYOUT_WAIT);
+      const int32_t* cnt =
+          reinterpret_cast<const int32_t*>(a.peer[s] + a.off_count + (size_t)parity * a.count_stride);
+      for (int e = tid; e < E; e += kLayoutThreads) {
+        int t = 0, b = 0;
+        for (int q = 0; q < P; ++q) {
+          const int val = ld_cg(cnt + (size_t)q * E + e);
+          t += val;
+          b += (q < s) ? val : 0;
+        }
+        tot[e] = t;
+        before[e] = b;
+      }
+    } else {
+      for (int e = tid; e < E; e += kLayoutThreads) {
+        tot[e] = ld_cg(totals + e);
+        before[e] = 0;
+      }
     }
     __syncthreads();
     // base_g(e): exclusive scan of totals over rank g's experts (one warp per rank)
@@ -236,13 +268,16 @@ __global__ void __launch_bounds__(kLayoutThreads)
     }
     __syncthreads();
     for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
-      // chunk offset within (rank s, expert e): Σ of the earlier chunks' counts
-      for (int e = tid; e < E; e += kLayoutThreads) {
-        int acc = 0;
+      if (c != c_first) {  // later chunks of this CTA (T > grid * 256)
+        __syncthreads();
+        for (int e = tid; e < E; e += kLayoutThreads) {
+          int acc = 0;
 #pragma unroll 8
-        for (int c2 = 0; c2 < c; ++c2) acc += ld_cg(a.chunk_cnt + (size_t)c2 * E + e);
-        pre[e] = base[e] + before[e] + acc;
+          for (int c2 = 0; c2 < c; ++c2) acc += ld_cg(a.chunk_cnt + (size_t)c2 * E + e);
+          pre[e] = acc;
+        }
       }
+      for (int e = tid; e < E; e += kLayoutThreads) pre[e] += base[e] + before[e];
       __syncthreads();
       const int t0 = c * kLayoutThreads;
       const int nel = min(kLayoutThreads, T - t0) * K;
@@ -254,7 +289,6 @@ __global__ void __launch_bounds__(kLayoutThreads)
         if (r >= a.max_rows) record_error(a.status, FS_ERANGE);
         row_of[base_el + j] = (int32_t)r;
       }
-      __syncthreads();
     }
     if (blockIdx.x == 0) {
       const int jb = a.seg_begin[s], je = a.seg_begin[s + 1];
@@ -334,6 +368,39 @@ __device__ __forceinline__ void warp_copy_row_cg(V* __restrict__ dst, const V* _
       const int w = w0 + j * 32 + lane;
       if (w < nv) st_na(dst + w, v[j]);
     }
+  }
+}
+
+// Receiver-side fan-out: rows whose fan_src points at another row (a
+// duplicate destination of a token that crossed NVLink once) are copied from
+// that primary row, in (row, slice) units spread over every warp of the grid
+// so a few duplicate-heavy row ranges cannot serialise on a few warps.
+template <typename V>
+__device__ __forceinline__ void fan_out_rows(const FsArgs& a, size_t act_off, size_t fan_off, int nv) {
+  constexpr int U = MoveCfg<V>::U;
+  constexpr int SW = 32 * U;
+  const int lane = threadIdx.x & 31;
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  const int rows = *reinterpret_cast<volatile int*>(a.num_rows);
+  const int S = (nv + SW - 1) / SW;
+  const int32_t* fs = reinterpret_cast<const int32_t*>(a.peer[a.rank] + fan_off);
+  V* act = reinterpret_cast<V*>(a.peer[a.rank] + act_off);
+  const long long units = (long long)rows * S;
+  for (long long u = gw; u < units; u += nw) {
+    const int r = (int)(u / S), sl = (int)(u - (long long)r * S);
+    const int f = ld_cg(fs + r);
+    if (f == r || f < 0 || f >= rows) continue;  // warp-uniform
+    const int w0 = sl * SW, rem = nv - w0;
+    const V* src = act + (size_t)f * nv + w0;
+    V* dst = act + (size_t)r * nv + w0;
+    V v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (j * 32 + lane < rem) v[j] = ld_cg(src + j * 32 + lane);
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (j * 32 + lane < rem) st_na(dst + j * 32 + lane, v[j]);
   }
 }
 
@@ -418,20 +485,7 @@ __global__ void __launch_bounds__(kMoveThreads)
       wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffArrive) + threadIdx.x, epoch, a);
     __syncthreads();
     trace_stamp(a, FS_TRACE_DISPATCH_ARRIVED);
-    const int rows = *reinterpret_cast<volatile int*>(a.num_rows);
-    const int32_t* fs = reinterpret_cast<const int32_t*>(a.peer[s] + fan_off);
-    V* act = reinterpret_cast<V*>(a.peer[s] + act_off);
-    for (int r0 = gw * 32; r0 < rows; r0 += nw * 32) {
-      const int r = r0 + lane;
-      const int f = r < rows ? ld_cg(fs + r) : r;
-      uint32_t need = __ballot_sync(kFull, r < rows && f != r && f >= 0 && f < rows);
-      while (need) {
-        const int d = __ffs(need) - 1;
-        need &= need - 1;
-        const int ff = __shfl_sync(kFull, f, d);
-        warp_copy_row_cg(act + (size_t)(r0 + d) * nv, act + (size_t)ff * nv, nv, lane);
-      }
-    }
+    fan_out_rows<V>(a, act_off, fan_off, nv);
   }
   trace_stamp(a, FS_TRACE_DISPATCH_END);
 }
@@ -535,23 +589,7 @@ __global__ void __launch_bounds__(kTmaThreads)
       wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffArrive) + threadIdx.x, epoch, a);
     __syncthreads();
     trace_stamp(a, FS_TRACE_DISPATCH_ARRIVED);
-    const int rows = *reinterpret_cast<volatile int*>(a.num_rows);
-    const int nv = tb / 16;
-    const int32_t* fs = reinterpret_cast<const int32_t*>(a.peer[s] + fan_off);
-    int4* act = reinterpret_cast<int4*>(a.peer[s] + act_off);
-    const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    const int nw = (int)((gridDim.x * blockDim.x) >> 5);
-    for (int r0 = gw * 32; r0 < rows; r0 += nw * 32) {
-      const int rr = r0 + lane;
-      const int f = rr < rows ? ld_cg(fs + rr) : rr;
-      uint32_t need = __ballot_sync(kFull, rr < rows && f != rr && f >= 0 && f < rows);
-      while (need) {
-        const int d = __ffs(need) - 1;
-        need &= need - 1;
-        const int ff = __shfl_sync(kFull, f, d);
-        warp_copy_row_cg(act + (size_t)(r0 + d) * nv, act + (size_t)ff * nv, nv, lane);
-      }
-    }
+    fan_out_rows<int4>(a, act_off, fan_off, tb / 16);
   }
   trace_stamp(a, FS_TRACE_DISPATCH_END);
 }
