@@ -80,9 +80,14 @@ def traffic(experts: np.ndarray, source: np.ndarray, owner: np.ndarray, P: int, 
     c_eg = np.bincount(own[remote], minlength=P) * tb          # rows pulled out of owner g
     c_in = np.bincount(source, weights=remote.sum(1), minlength=P) * tb
     rows = np.bincount(own.reshape(-1), minlength=P)
-    # HBM bytes of each kernel on each rank (reads + writes of payload rows)
-    dedup_rows_in = np.bincount(own[send], minlength=P)
-    hbm_disp = T_l * tb + rows * tb + (rows - dedup_rows_in) * tb * (P > 1)  # read x, write rows (+fan-out read)
+    # HBM bytes of each kernel on each rank (reads + writes of payload rows):
+    # dispatch reads x, every received row is written once, and each duplicate
+    # of a remote token is fanned out from its primary row (one more read);
+    # combine reads every row once (at its owner) and writes the outputs.
+    local_rows = np.bincount(own[~remote], minlength=P)
+    primaries_in = np.bincount(own[send], minlength=P)
+    dups = rows - local_rows - primaries_in
+    hbm_disp = T_l * tb + rows * tb + dups * tb
     hbm_comb = rows * tb + T_l * tb
     return dict(d_eg=d_eg, d_in=d_in, c_eg=c_eg, c_in=c_in, rows=rows, hbm_disp=hbm_disp, hbm_comb=hbm_comb)
 
@@ -148,9 +153,9 @@ def parse():
     ap.add_argument("--soak-s", type=float, default=1.5, help="untimed load before timing (clock ramp, sampling)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--graph", action="store_true", help="time K steps as CUDA-graph replays")
-    ap.add_argument("--dispatch", choices=["warp", "tma"], default=os.environ.get("FUSCO_DISPATCH", "warp"),
+    ap.add_argument("--dispatch", choices=["warp", "tma"], default=os.environ.get("FUSCO_DISPATCH", "tma"),
                     help="dispatch data mover: warp LDG/STG loop or TMA bulk copies")
-    ap.add_argument("--combine", choices=["warp", "tma"], default=os.environ.get("FUSCO_COMBINE", "warp"),
+    ap.add_argument("--combine", choices=["warp", "tma"], default=os.environ.get("FUSCO_COMBINE", "tma"),
                     help="combine data mover: warp LDG loop or TMA bulk loads into smem stages")
     return ap.parse_args()
 
@@ -427,9 +432,12 @@ def main() -> int:
                 "frac": achieved / pk["hbm"], "peak_src": pk["hbm_src"], "bytes_per_launch": b,
                 "traffic": None}
     else:
+        # bottleneck rank's NVLink bytes (max of egress / ingress over ranks);
+        # the kernel floor is the slower of that over the link and its HBM bytes
         d_bn = float(np.maximum(tr["d_eg"], tr["d_in"]).max())
         c_bn = float(np.maximum(tr["c_eg"], tr["c_in"]).max())
-        t_min_d, t_min_c = d_bn / (NVLINK_NOMINAL * 1e9), c_bn / (NVLINK_NOMINAL * 1e9)
+        t_min_d = max(d_bn / (NVLINK_NOMINAL * 1e9), float(tr["hbm_disp"].max()) / (pk["hbm"] * 1e9))
+        t_min_c = max(c_bn / (NVLINK_NOMINAL * 1e9), float(tr["hbm_comb"].max()) / (pk["hbm"] * 1e9))
         dom = "fs_dispatch" if k_disp >= k_comb else "fs_combine"
         b, t = (d_bn, k_disp) if dom == "fs_dispatch" else (c_bn, k_comb)
         achieved = b / (t * 1e-3) / 1e9

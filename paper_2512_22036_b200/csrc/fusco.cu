@@ -276,12 +276,15 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
   h->move_grid = grid_ctas > 0 ? std::min(grid_ctas, occ_d * sms) : occ_d * sms;
   // TMA engine: ~100 KB of row slots per CTA, two CTAs per SM
   {
+    // default engine: TMA (measured best or equal on B200 across the
+    // BASELINE configs); FUSCO_DISPATCH=warp selects the LDG/STG mover
     const char* mode = getenv("FUSCO_DISPATCH");
-    h->dispatch_tma = (mode && std::string(mode) == "tma" && token_bytes % 16 == 0) ? 1 : 0;
+    const bool want_tma = !(mode && std::string(mode) == "warp");
+    h->dispatch_tma = (want_tma && token_bytes % 16 == 0) ? 1 : 0;
     const char* lag = getenv("FUSCO_TMA_LAG");
     h->tma_lag = (lag && atoi(lag) >= 4) ? 4 : 2;
     const char* ctas = getenv("FUSCO_TMA_CTAS");
-    h->tma_ctas = ctas ? std::max(1, std::min(8, atoi(ctas))) : 2;
+    h->tma_ctas = ctas ? std::max(1, std::min(8, atoi(ctas))) : 3;
     const int slot = tma_slot_bytes(token_bytes);
     h->tma_slots = std::max(h->tma_lag + 2, std::min(kTmaMaxSlots, (int)((200 * 1024 / h->tma_ctas - 512) / slot)));
     h->tma_smem = 2 * kTmaMaxSlots * sizeof(uint64_t) + (size_t)h->tma_slots * slot;
@@ -301,11 +304,12 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
   // TMA combine: ~100 KB of [K][slice] stages per CTA, two CTAs per SM
   {
     const char* mode = getenv("FUSCO_COMBINE");
-    h->combine_tma = (mode && std::string(mode) == "tma" && token_bytes % 16 == 0) ? 1 : 0;
+    const bool want_tma = !(mode && std::string(mode) == "warp");
+    h->combine_tma = (want_tma && token_bytes % 16 == 0) ? 1 : 0;
     h->comb_sb = comb_slice_bytes(token_bytes, topk);
     const int stage = topk * h->comb_sb;
     const char* cctas = getenv("FUSCO_TMA_CTAS");
-    const int comb_ctas = cctas ? std::max(1, std::min(8, atoi(cctas))) : 2;
+    const int comb_ctas = cctas ? std::max(1, std::min(8, atoi(cctas))) : 3;
     h->comb_stages = std::max(2, std::min(kCombMaxStages, (200 * 1024 / comb_ctas) / stage));
     h->comb_smem = 2 * kCombMaxStages * sizeof(uint64_t) + (size_t)h->comb_stages * stage;
     h->comb_grid = 0;
@@ -446,8 +450,7 @@ int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_byte
   FsArgs a = make_args(h, num_tokens, idx_bytes == 8);
   const bool vec16 = (h->tb % 16 == 0) && aligned(x, 16);
   if (!aligned(x, 4)) return fail(FS_EINVAL, "x must be 4-byte aligned");
-  if (h->dispatch_tma) {
-    if (!vec16) return fail(FS_EINVAL, "TMA dispatch needs 16-byte aligned rows");
+  if (h->dispatch_tma && vec16) {  // unaligned x falls back to the warp mover (same grid)
     int nslots = h->tma_slots;
     void* targs[] = {&a, (void*)&x, (void*)&topk_idx, (void*)&row_of, &phase, &nslots};
     const void* tfn = h->tma_lag == 4 ? (const void*)dispatch_tma_kernel<4> : (const void*)dispatch_tma_kernel<2>;
