@@ -152,7 +152,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--soak-s", type=float, default=1.5, help="untimed load before timing (clock ramp, sampling)")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--graph", action="store_true", help="time K steps as CUDA-graph replays")
+    ap.add_argument("--graph", action="store_true", default=True,
+                    help="time K steps as CUDA-graph replays (default; per-kernel split from an eager pass)")
+    ap.add_argument("--eager", dest="graph", action="store_false", help="time K eager launches instead")
     ap.add_argument("--dispatch", choices=["warp", "tma"], default=os.environ.get("FUSCO_DISPATCH", "tma"),
                     help="dispatch data mover: warp LDG/STG loop or TMA bulk copies")
     ap.add_argument("--combine", choices=["warp", "tma"], default=os.environ.get("FUSCO_COMBINE", "tma"),
