@@ -431,13 +431,9 @@ class EPBuffer:
         call("fs_sym_alloc", self.device.index, nbytes, byref(own))
         handle = (ctypes.c_uint8 * 64)()
         call("fs_ipc_handle", self.device.index, own, handle)
-        gather = exchange or exchange_objects
-        infos = gather((bytes(handle), cfg, self.rank_id), group)
-        for h, c, r in infos:
-            if c != cfg:
-                raise ValueError(f"rank {r} shuffle configuration differs from rank {self.rank_id}")
+        infos = bootstrap_exchange(bytes(handle), cfg, self.rank_id, group, exchange)
         self._peers = _Peers()
-        for g, (h, _, _) in enumerate(infos):
+        for g, h in enumerate(infos):
             if g == self.rank_id:
                 self._peers.regions.append(own.value)
                 continue
@@ -497,6 +493,23 @@ class EPBuffer:
         for p in self._peers.opened:
             lib.fs_ipc_close(self.device.index, c_void_p(p))
         lib.fs_sym_free(self.device.index, c_void_p(self._own))
+
+
+def bootstrap_exchange(handle: bytes, cfg: tuple, rank: int, group=None, exchange=None) -> list[bytes]:
+    """All-gather every rank's 64-byte region handle together with its shuffle
+    configuration; every rank must agree on the configuration (the symmetric
+    regions have identical layouts), else ValueError on every rank.  Returns the
+    handles in rank order."""
+    gather = exchange or exchange_objects
+    infos = gather((bytes(handle), cfg, rank), group)
+    for i, (h, c, r) in enumerate(infos):
+        if r != i:
+            raise ValueError(f"bootstrap: slot {i} answered by rank {r}")
+        if c != cfg:
+            raise ValueError(f"rank {r} shuffle configuration differs from rank {rank}")
+        if len(h) != 64:
+            raise ValueError(f"rank {r} sent a malformed region handle")
+    return [h for h, _, _ in infos]
 
 
 def exchange_objects(obj, group=None) -> list:
