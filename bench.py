@@ -147,7 +147,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
-    ap.add_argument("--impl", default="fusco", choices=["fusco", "reference"])
+    ap.add_argument("--impl", default="fusco", choices=["fusco", "reference", "nccl"],
+                    help="fusco (this repo), reference (CPU oracle port), nccl (disaggregated GPU baseline)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--soak-s", type=float, default=1.5, help="untimed load before timing (clock ramp, sampling)")
@@ -215,6 +216,56 @@ def cpu_reference(cfg_name: str, P: int, seed: int, steps: int, warmup: int, bud
     }
 
 
+def run_nccl_baseline(args, world, rank, local, dev) -> int:
+    """Disaggregated pack / NCCL all-to-all / unpack on the same config (§8f #1)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_22036_b200.baseline import DisaggregatedShuffle
+
+    hidden, dtype, E, K, T_l, zipf, desc = CONFIGS[args.config]
+    a, pl = routing_for(args.config, world, args.seed)
+    ids = np.flatnonzero(a.source == rank)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    tb = hidden * (2 if dtype == "bf16" else 4)
+    x = torch.randn(T_l, hidden, device=dev).to(tdt)
+    idx = torch.as_tensor(a.experts[ids], device=dev)
+    w = torch.as_tensor(a.weights[ids], dtype=torch.float32, device=dev)
+    base = DisaggregatedShuffle(num_experts=E, topk=K, device=dev)
+
+    def step():
+        act, st = base.dispatch(x, idx)
+        return base.combine(act, st, w)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(args.steps):
+        step()
+    s1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([s0.elapsed_time(s1) / args.steps], device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    routed = 2.0 * world * T_l * K * tb
+    line = {"impl": "nccl", "metric": METRIC, "value": routed / (ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "latency_us": ms * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": {"workload": desc, "ep": world},
+            "rearrange_bytes_per_rank": DisaggregatedShuffle.rearrange_bytes(T_l, K, tb)}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def main() -> int:
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -248,6 +299,8 @@ def main() -> int:
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    if args.impl == "nccl":
+        return run_nccl_baseline(args, world, rank, local, dev)
     P = world
     a, pl = routing_for(args.config, P, args.seed)
     elem = 2 if dtype == "bf16" else 4

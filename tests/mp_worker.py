@@ -16,6 +16,7 @@ sys.path.insert(0, str(ROOT))
 
 from oracle import shuffle_oracle as O  # noqa: E402
 from paper_2512_22036_b200 import EPBuffer, box, gen_realworld, round_robin_placement  # noqa: E402
+from paper_2512_22036_b200.baseline import DisaggregatedShuffle  # noqa: E402
 
 
 def main() -> int:
@@ -27,6 +28,7 @@ def main() -> int:
     topo = box(P)
     pl = round_robin_placement(E, topo)
     buf = EPBuffer(num_experts=E, topk=K, hidden=H, dtype="bf16", max_tokens=T_l, timeout_ms=20000)
+    base = DisaggregatedShuffle(num_experts=E, topk=K)
     dev = torch.device("cuda", local)
     failures = 0
     for it in range(4):
@@ -58,6 +60,16 @@ def main() -> int:
         want = O.combine(acts, row_of, a.experts, a.weights, pl.owner, ids, "bf16")
         if not np.array_equal(out.view(torch.uint8).cpu().numpy(), want):
             print(f"[rank {rank}] iter {it}: output mismatch", flush=True)
+            failures += 1
+        # disaggregated NCCL baseline: same activation bytes, outputs within bf16 tolerance
+        bact, st = base.dispatch(x, idx)
+        if not torch.equal(bact.view(torch.uint8), act[:rows].view(torch.uint8)):
+            print(f"[rank {rank}] iter {it}: baseline activation differs from fused", flush=True)
+            failures += 1
+        bout = base.combine(bact, st, w.float())
+        ref = torch.as_tensor(O.decode(want, "bf16"), device=dev)
+        if not torch.allclose(bout.float(), ref, rtol=2.0**-8, atol=1e-3):
+            print(f"[rank {rank}] iter {it}: baseline output out of tolerance", flush=True)
             failures += 1
     t = torch.tensor([failures], device=dev)
     dist.all_reduce(t)

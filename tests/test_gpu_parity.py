@@ -334,3 +334,19 @@ def test_device_errors_raise_value_error():
         ok = [torch.tensor([[0, 1]], device=dev), torch.tensor([[1, 2]], device=dev)]
         cl.layout(ok)
         cl.check()
+
+
+def test_disaggregated_baseline_single_gpu_matches_fused():
+    """§8f next row: the pack/all-to-all/unpack baseline lands the same bytes."""
+    from paper_2512_22036_b200.baseline import DisaggregatedShuffle
+
+    pkg, topo, pl, a, tb, payload = _cluster_case(1, 32, 4, 700, 1024, "bf16", 0.8, seed=21)
+    res = _run_cluster(pkg, topo, pl, a, tb, payload, "bf16", "f64")
+    dev = torch.device("cuda", 0)
+    base = DisaggregatedShuffle(num_experts=32, topk=4, device=dev)
+    x = torch.as_tensor(payload, device=dev).view(torch.bfloat16)
+    act, st = base.dispatch(x, torch.as_tensor(a.experts, device=dev))
+    assert np.array_equal(act.view(torch.uint8).cpu().numpy(), res["acts"][0])
+    out = base.combine(act, st, torch.as_tensor(a.weights, dtype=torch.float32, device=dev))
+    np.testing.assert_allclose(out.float().cpu().numpy(), O.decode(res["outs"][0], "bf16"), **BF16_TOL)
+    assert base.rearrange_bytes(700, 4, tb) == 4 * 700 * 4 * tb
