@@ -626,8 +626,10 @@ __device__ __forceinline__ double fma_acc<double>(double w, float y, double acc)
 }
 
 __device__ __forceinline__ uint32_t pack_out(float lo, float hi) {
-  const __nv_bfloat16 a = __float2bfloat16_rn(lo), b = __float2bfloat16_rn(hi);
-  return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
+  // one cvt.rn.bf16x2.f32 (round-to-nearest-even, same as two __float2bfloat16_rn)
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
 }
 __device__ __forceinline__ uint32_t pack_out(double lo, double hi) {
   const __nv_bfloat16 a = __double2bfloat16(lo), b = __double2bfloat16(hi);
@@ -769,7 +771,7 @@ __global__ void __launch_bounds__(kMoveThreads)
 // consumer warp arrives on empty[q] when done.  Loads in flight per SM = NS
 // stages of K·SB bytes, independent of register pressure.
 // ===========================================================================
-constexpr int kCombConsumers = 4;
+constexpr int kCombConsumers = 8;
 constexpr int kCombThreads = 32 * (1 + kCombConsumers);
 constexpr int kCombMaxStages = 16;
 constexpr int kCombStageTarget = 24 * 1024;  // bytes of one stage (K row slices)
