@@ -156,9 +156,9 @@ def parse():
     ap.add_argument("--graph", action="store_true", default=True,
                     help="time K steps as CUDA-graph replays (default; per-kernel split from an eager pass)")
     ap.add_argument("--eager", dest="graph", action="store_false", help="time K eager launches instead")
-    ap.add_argument("--dispatch", choices=["warp", "tma"], default=os.environ.get("FUSCO_DISPATCH", "tma"),
+    ap.add_argument("--dispatch", choices=["warp", "tma", "auto"], default=os.environ.get("FUSCO_DISPATCH", "auto"),
                     help="dispatch data mover: warp LDG/STG loop or TMA bulk copies")
-    ap.add_argument("--combine", choices=["warp", "tma"], default=os.environ.get("FUSCO_COMBINE", "tma"),
+    ap.add_argument("--combine", choices=["warp", "tma", "auto"], default=os.environ.get("FUSCO_COMBINE", "auto"),
                     help="combine data mover: warp LDG loop or TMA bulk loads into smem stages")
     return ap.parse_args()
 
@@ -543,8 +543,8 @@ def main() -> int:
         "roofline": roof,
         "gpu_launches": launches,
         "launch_mode": "cuda_graph" if graph is not None else "eager",
-        "dispatch_engine": args.dispatch,
-        "combine_engine": args.combine,
+        "dispatch_engine": args.dispatch if args.dispatch != "auto" else ("tma" if P == 1 else "warp"),
+        "combine_engine": args.combine if args.combine != "auto" else ("warp" if P == 1 else "tma"),
         "host_enqueue_ms_per_step": host_ms / args.steps,
         "clocks": clocks,
     }

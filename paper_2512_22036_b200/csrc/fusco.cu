@@ -63,6 +63,8 @@ struct fs_ctx {
   int tma_slots;        // smem ring slots per CTA of the TMA engine
   int tma_lag, tma_ctas;
   size_t tma_smem;
+  int cluster_layout;   // 1: single-cluster DSMEM planner usable (E <= 256, K <= 8)
+  size_t cluster_smem;
   int combine_tma;      // 1: TMA combine engine (FUSCO_COMBINE=tma)
   int comb_sb, comb_stages, comb_grid;
   size_t comb_smem;
@@ -276,10 +278,12 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
   h->move_grid = grid_ctas > 0 ? std::min(grid_ctas, occ_d * sms) : occ_d * sms;
   // TMA engine: ~100 KB of row slots per CTA, two CTAs per SM
   {
-    // default engine: TMA (measured best or equal on B200 across the
-    // BASELINE configs); FUSCO_DISPATCH=warp selects the LDG/STG mover
+    // Engine selection (FUSCO_DISPATCH = tma | warp | auto, default auto).
+    // Measured on B200: TMA wins the HBM-bound single-rank permutation, the
+    // warp mover wins when pushes go over NVLink (profiles/).
     const char* mode = getenv("FUSCO_DISPATCH");
-    const bool want_tma = !(mode && std::string(mode) == "warp");
+    const std::string dm = mode ? std::string(mode) : std::string("auto");
+    const bool want_tma = dm == "tma" || (dm == "auto" && world == 1);
     h->dispatch_tma = (want_tma && token_bytes % 16 == 0) ? 1 : 0;
     const char* lag = getenv("FUSCO_TMA_LAG");
     h->tma_lag = (lag && atoi(lag) >= 4) ? 4 : 2;
@@ -301,10 +305,23 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
     }
   }
   h->sms = sms;
+  {
+    const char* lm = getenv("FUSCO_LAYOUT");  // cluster (default) | grid
+    h->cluster_layout = !(lm && std::string(lm) == "grid") && num_experts <= kClusterMaxE && topk <= kClusterMaxK;
+    h->cluster_smem = layout_cluster_smem_bytes(num_experts, topk);
+    if (h->cluster_layout) {
+      e = cudaFuncSetAttribute(layout_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->cluster_smem);
+      if (e != cudaSuccess) h->cluster_layout = 0;  // fall back to the grid planner
+      cudaGetLastError();
+    }
+  }
   // TMA combine: ~100 KB of [K][slice] stages per CTA, two CTAs per SM
   {
+    // FUSCO_COMBINE = tma | warp | auto (default): warp pull for the local
+    // (HBM) case, TMA stages for NVLink pulls (measured)
     const char* mode = getenv("FUSCO_COMBINE");
-    const bool want_tma = !(mode && std::string(mode) == "warp");
+    const std::string cm = mode ? std::string(mode) : std::string("auto");
+    const bool want_tma = cm == "tma" || (cm == "auto" && world > 1);
     h->combine_tma = (want_tma && token_bytes % 16 == 0) ? 1 : 0;
     h->comb_sb = comb_slice_bytes(token_bytes, topk);
     const int stage = topk * h->comb_sb;
@@ -427,11 +444,30 @@ int fs_layout(fs_handle_t h, const void* topk_idx, int idx_bytes, int num_tokens
   if (num_tokens > 0 && (!topk_idx || !row_of)) return fail(FS_EINVAL, "null topk_idx / row_of");
   if (phase & FS_PHASE_LOCAL) h->epoch++;
   FsArgs a = make_args(h, num_tokens, idx_bytes == 8);
+  long long* st_ptr = reinterpret_cast<long long*>(stats);
+  const int ncl = (num_tokens + kClusterThreads - 1) / kClusterThreads;
+  if (phase == FS_PHASE_ALL && h->cluster_layout && ncl <= kClusterMaxCtas) {
+    const int cs = std::max(1, ncl);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = h->cluster_smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FS_CUDA(cudaLaunchKernelEx(&cfg, layout_cluster_kernel, a, topk_idx, row_of, first_mask, rank_mask, st_ptr,
+                               expert_counts, expert_offsets));
+    return FS_OK;
+  }
   const int nchunks = (num_tokens + kLayoutThreads - 1) / kLayoutThreads;
   const int grid = std::max(1, std::min(nchunks, h->layout_grid_max));
-  long long* st = reinterpret_cast<long long*>(stats);
   void* args[] = {&a, (void*)&topk_idx, &row_of, &first_mask, &rank_mask,
-                  &st, &expert_counts, &expert_offsets, &phase};
+                  &st_ptr, &expert_counts, &expert_offsets, &phase};
   FS_CUDA(cudaLaunchCooperativeKernel((const void*)layout_kernel, dim3(grid), dim3(kLayoutThreads), args,
                                       h->layout_smem, (cudaStream_t)stream));
   return FS_OK;

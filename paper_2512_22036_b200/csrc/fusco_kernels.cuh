@@ -309,6 +309,238 @@ __global__ void __launch_bounds__(kLayoutThreads)
 }
 
 // ===========================================================================
+// Layout planner, cluster engine (production, one launch for both phases)
+//
+// For E <= 256, K <= 8, T <= 8 x 1024: ONE thread-block cluster of CS <= 8
+// CTAs x 1024 threads, one token per thread.  Each CTA builds its chunk's
+// per-expert counts and in-chunk positions exactly as layout_kernel does
+// (warp bitmasks, 32 warps), then the chunk offsets and per-expert totals come
+// from the other CTAs' shared memory over DSMEM after one cluster barrier —
+// no global atomics, no cooperative grid barrier.  Cluster rank 0 publishes
+// the totals to the peers (P > 1).
+// ===========================================================================
+constexpr int kClusterThreads = 1024;
+constexpr int kClusterWarps = kClusterThreads / 32;
+constexpr int kClusterMaxCtas = 8;
+constexpr int kClusterMaxE = 256;
+constexpr int kClusterMaxK = 8;
+
+__host__ __device__ inline size_t layout_cluster_smem_bytes(int E, int K) {
+  // owner[E] node[32] bits[32][E] wbase[32][E] e_s[1024K] pos_s[1024K] cnt[E] tot/base/before/pre[4E]
+  return sizeof(int32_t) * ((size_t)E + 32 + 2ull * kClusterWarps * E + 2ull * kClusterThreads * K + 5ull * E);
+}
+
+__global__ void __launch_bounds__(kClusterThreads, 1)
+    layout_cluster_kernel(FsArgs a, const void* __restrict__ idx, int32_t* __restrict__ row_of,
+                          uint8_t* __restrict__ first_mask, uint32_t* __restrict__ rank_mask,
+                          long long* __restrict__ stats, int32_t* __restrict__ expert_counts,
+                          int32_t* __restrict__ expert_offsets) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  __shared__ long long red[kClusterWarps][4];
+  __shared__ long long cta_stats[4];
+  __shared__ int rows_total;
+  const int E = a.E, K = a.K, T = a.T, P = a.world, s = a.rank;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t crank = cluster_ctarank();
+  const int CS = (int)gridDim.x;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const uint32_t epoch = load_epoch(a) + 1u;
+  const int parity = (int)(epoch & 1u);
+  trace_stamp(a, FS_TRACE_LAYOUT_BEGIN);
+
+  int32_t* owner_s = reinterpret_cast<int32_t*>(sm);
+  int32_t* node_s = owner_s + E;
+  uint32_t* bits = reinterpret_cast<uint32_t*>(node_s + 32);   // [32][E]
+  uint32_t* wbase = bits + kClusterWarps * E;                   // [32][E]
+  int32_t* e_s = reinterpret_cast<int32_t*>(wbase + kClusterWarps * E);
+  int32_t* pos_s = e_s + kClusterThreads * K;
+  int32_t* cnt = pos_s + kClusterThreads * K;                   // this CTA's per-expert counts
+  int32_t* tot = cnt + E;
+  int32_t* base = tot + E;
+  int32_t* before = base + E;
+  int32_t* pre = before + E;
+
+  const int t0 = (int)crank * kClusterThreads;
+  const int ntok = max(0, min(kClusterThreads, T - t0));
+  const int nel = ntok * K;
+  const size_t base_el = (size_t)t0 * K;
+  // one round trip: expert table, node table and this CTA's indices together
+  for (int e = tid; e < E; e += kClusterThreads) owner_s[e] = a.owner[e];
+  if (tid < P) node_s[tid] = a.node_of[tid];
+  for (int j = tid; j < nel; j += kClusterThreads) {
+    long long e = load_idx(idx, base_el + j, a.idx64);
+    if (e < 0 || e >= E) {
+      record_error(a.status, FS_ERANGE);
+      e = 0;
+    }
+    e_s[j] = (int32_t)e;
+  }
+  for (int j = tid; j < kClusterWarps * E; j += kClusterThreads) bits[j] = 0u;
+  if (tid < 4) cta_stats[tid] = 0;
+  __syncthreads();
+
+  long long st_dedup = 0, st_naive = 0, st_local = 0, st_node = 0;
+  if (tid < ntok) {
+    const int my_node = node_s[s];
+    uint32_t seen_node = 0u, seen_rank = 0u;
+    for (int k = 0; k < K; ++k) {
+      const int e = e_s[tid * K + k];
+      const int g = owner_s[e];
+      const int n = node_s[g];
+      const bool first = !((seen_node >> n) & 1u);
+      seen_node |= 1u << n;
+      seen_rank |= 1u << g;
+      pos_s[tid * K + k] = first ? 1 : 0;
+      st_naive += (g != s);
+      st_local += (g == s);
+      st_node += (first && n != my_node);
+      const uint32_t old = atomicOr(&bits[warp * E + e], 1u << lane);
+      if (old & (1u << lane)) record_error(a.status, FS_EINVAL);
+    }
+    if (rank_mask) rank_mask[t0 + tid] = seen_rank;
+    st_dedup += __popc(seen_rank & ~(1u << s));
+  }
+  {
+    long long v[4] = {st_dedup, st_naive, st_local, st_node};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_xor_sync(kFull, v[j], o);
+      if (lane == 0) red[warp][j] = v[j];
+    }
+  }
+  __syncthreads();
+  if (first_mask)
+    for (int j = tid; j < nel; j += kClusterThreads) first_mask[base_el + j] = (uint8_t)pos_s[j];
+  if (tid < 4) {
+    long long acc = 0;
+    for (int w = 0; w < kClusterWarps; ++w) acc += red[w][tid];
+    cta_stats[tid] = acc;
+  }
+  // per-expert warp prefixes: 8 warps x 32 lanes cover the experts, each lane
+  // walks the 32 warps' words of its expert
+  for (int e = tid; e < E; e += kClusterThreads) {
+    uint32_t run = 0;
+#pragma unroll 8
+    for (int w = 0; w < kClusterWarps; ++w) {
+      wbase[w * E + e] = run;
+      run += __popc(bits[w * E + e]);
+    }
+    cnt[e] = (int32_t)run;
+  }
+  __syncthreads();
+  if (tid < ntok)
+    for (int k = 0; k < K; ++k) {
+      const int e = e_s[tid * K + k];
+      pos_s[tid * K + k] = (int32_t)(wbase[warp * E + e] + __popc(bits[warp * E + e] & lt_mask));
+    }
+  trace_stamp(a, FS_TRACE_LAYOUT_HIST);
+  cluster_sync_all();  // every CTA's cnt[] and cta_stats[] are final
+  trace_stamp(a, FS_TRACE_LAYOUT_GRIDSYNC);
+
+  // chunk offset (earlier CTAs) and rank totals from the cluster's smem
+  for (int e = tid; e < E; e += kClusterThreads) {
+    int p_acc = 0, t_acc = 0;
+    for (int r = 0; r < CS; ++r) {
+      const int v = (r == (int)crank) ? cnt[e] : (int)ld_dsmem_u32(&cnt[e], (uint32_t)r);
+      t_acc += v;
+      p_acc += (r < (int)crank) ? v : 0;
+    }
+    pre[e] = p_acc;
+    tot[e] = t_acc;
+  }
+  __syncthreads();
+  if (crank == 0) {
+    if (P > 1) {
+      for (int e = tid; e < E; e += kClusterThreads)
+        for (int g = 0; g < P; ++g) {
+          int32_t* dst = reinterpret_cast<int32_t*>(a.peer[g] + a.off_count + (size_t)parity * a.count_stride);
+          dst[(size_t)s * E + e] = tot[e];
+        }
+    }
+    if (stats && tid < 4) {
+      long long acc = 0;
+      for (int r = 0; r < CS; ++r) {
+        const uint32_t lo = (r == 0) ? (uint32_t)(cta_stats[tid] & 0xffffffffu)
+                                     : ld_dsmem_u32(reinterpret_cast<const uint32_t*>(&cta_stats[tid]), r);
+        const uint32_t hi = (r == 0) ? (uint32_t)((unsigned long long)cta_stats[tid] >> 32)
+                                     : ld_dsmem_u32(reinterpret_cast<const uint32_t*>(&cta_stats[tid]) + 1, r);
+        acc += (long long)(((unsigned long long)hi << 32) | lo);
+      }
+      const int slot[4] = {FS_STAT_DEDUP_SEND, FS_STAT_NAIVE_SEND, FS_STAT_LOCAL_ROWS, FS_STAT_NODE_DEDUP};
+      stats[slot[tid]] = acc;
+    }
+    if (stats && tid >= 5 && tid < FS_NSTATS) stats[tid] = 0;
+    if (tid == 0) *a.epoch_ptr = epoch;  // every CTA read the old epoch before the cluster barrier
+    if (P > 1) {
+      __syncthreads();
+      if (tid < P)
+        st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[tid] + kOffCountFlag) + s, epoch);
+    }
+    trace_stamp(a, FS_TRACE_LAYOUT_PUBLISH);
+  }
+
+  if (P > 1) {
+    if (tid < P)
+      wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffCountFlag) + tid, epoch, a);
+    __syncthreads();
+    trace_stamp(a, FS_TRACE_LAYOUT_WAIT);
+    const int32_t* cm =
+        reinterpret_cast<const int32_t*>(a.peer[s] + a.off_count + (size_t)parity * a.count_stride);
+    for (int e = tid; e < E; e += kClusterThreads) {
+      int t = 0, b = 0;
+      for (int q = 0; q < P; ++q) {
+        const int val = ld_cg(cm + (size_t)q * E + e);
+        t += val;
+        b += (q < s) ? val : 0;
+      }
+      tot[e] = t;
+      before[e] = b;
+    }
+  } else {
+    for (int e = tid; e < E; e += kClusterThreads) before[e] = 0;
+  }
+  __syncthreads();
+  for (int g = warp; g < P; g += kClusterWarps) {
+    int run = 0;
+    const int jb = a.seg_begin[g], je = a.seg_begin[g + 1];
+    for (int j0 = jb; j0 < je; j0 += 32) {
+      const int j = j0 + lane;
+      const int e = j < je ? a.perm[j] : -1;
+      const int val = e >= 0 ? tot[e] : 0;
+      const int incl = warp_incl_scan(val, lane);
+      if (e >= 0) base[e] = run + incl - val;
+      run += __shfl_sync(kFull, incl, 31);
+    }
+    if (g == s && lane == 0) rows_total = run;
+  }
+  __syncthreads();
+  for (int e = tid; e < E; e += kClusterThreads) pre[e] += base[e] + before[e];
+  __syncthreads();
+  for (int j = tid; j < nel; j += kClusterThreads) {
+    const long long r = (long long)pos_s[j] + pre[e_s[j]];
+    if (r >= a.max_rows) record_error(a.status, FS_ERANGE);
+    row_of[base_el + j] = (int32_t)r;
+  }
+  if (crank == 0) {
+    const int jb = a.seg_begin[s], je = a.seg_begin[s + 1];
+    for (int j = jb + tid; j < je; j += kClusterThreads) {
+      const int e = a.perm[j];
+      if (expert_counts) expert_counts[j - jb] = tot[e];
+      if (expert_offsets) expert_offsets[j - jb] = base[e];
+    }
+    if (tid == 0) {
+      if (expert_offsets) expert_offsets[je - jb] = rows_total;
+      *a.num_rows = rows_total;
+      if (stats) stats[FS_STAT_ROWS] = rows_total;
+      trace_stamp(a, FS_TRACE_LAYOUT_END);
+      if (rows_total > a.max_rows) record_error(a.status, FS_ERANGE);
+    }
+  }
+  cluster_sync_all();  // keep every CTA's shared memory alive until all DSMEM reads are done
+}
+
+// ===========================================================================
 // Dispatch
 //
 // Work unit = (token, slice of SLICE = 32 lanes x U vector words).  Lane k<K

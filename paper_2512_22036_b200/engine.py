@@ -347,25 +347,28 @@ class EmulatedCluster:
         except Exception:
             pass
 
+    # A single rank has no peer to wait for: it runs the production launches
+    # (FS_PHASE_ALL, e.g. the one-cluster planner).  P > 1 runs every rank's
+    # LOCAL phase, then every rank's REMOTE phase.
+    def _phases(self):
+        return (FS_PHASE_ALL,) if self.world == 1 else (FS_PHASE_LOCAL, FS_PHASE_REMOTE)
+
     def layout(self, topk_idx: list[torch.Tensor], with_masks: bool = True) -> list[Plan]:
         plans = [r.new_plan(t, with_masks) for r, t in zip(self.ranks, topk_idx)]
-        for r, p in zip(self.ranks, plans):
-            r.layout(p, FS_PHASE_LOCAL)
-        for r, p in zip(self.ranks, plans):
-            r.layout(p, FS_PHASE_REMOTE)
+        for ph in self._phases():
+            for r, p in zip(self.ranks, plans):
+                r.layout(p, ph)
         return plans
 
     def dispatch(self, xs: list[torch.Tensor], plans: list[Plan]) -> None:
-        for r, x, p in zip(self.ranks, xs, plans):
-            r.dispatch(x, p, FS_PHASE_LOCAL)
-        for r, x, p in zip(self.ranks, xs, plans):
-            r.dispatch(x, p, FS_PHASE_REMOTE)
+        for ph in self._phases():
+            for r, x, p in zip(self.ranks, xs, plans):
+                r.dispatch(x, p, ph)
 
     def combine(self, plans, ws, outs, *, dtype_code: int, src: int = FS_SRC_ACT, acc: int = FS_ACC_F32):
-        for r, p, w, o in zip(self.ranks, plans, ws, outs):
-            r.combine(p, w, o, dtype_code=dtype_code, src=src, acc=acc, phase=FS_PHASE_LOCAL)
-        for r, p, w, o in zip(self.ranks, plans, ws, outs):
-            r.combine(p, w, o, dtype_code=dtype_code, src=src, acc=acc, phase=FS_PHASE_REMOTE)
+        for ph in self._phases():
+            for r, p, w, o in zip(self.ranks, plans, ws, outs):
+                r.combine(p, w, o, dtype_code=dtype_code, src=src, acc=acc, phase=ph)
 
     def check(self) -> None:
         for r in self.ranks:

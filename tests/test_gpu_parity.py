@@ -350,3 +350,27 @@ def test_disaggregated_baseline_single_gpu_matches_fused():
     out = base.combine(act, st, torch.as_tensor(a.weights, dtype=torch.float32, device=dev))
     np.testing.assert_allclose(out.float().cpu().numpy(), O.decode(res["outs"][0], "bf16"), **BF16_TOL)
     assert base.rearrange_bytes(700, 4, tb) == 4 * 700 * 4 * tb
+
+
+@pytest.mark.parametrize("planner", ["cluster", "grid"])
+@pytest.mark.parametrize("E,K,T,zipf", [(8, 2, 8192, 0.0), (256, 8, 4096, 1.2), (64, 4, 1000, 0.5), (16, 3, 1, 0.0),
+                                        (256, 8, 7777, 0.0), (512, 8, 600, 0.0), (32, 12, 300, 0.0)])
+def test_planner_engines_single_rank(monkeypatch, planner, E, K, T, zipf):
+    """One-cluster DSMEM planner (E <= 256, K <= 8, T <= 8192) and the grid
+    planner give the reference layout (larger E/K fall back to the grid one)."""
+    monkeypatch.setenv("FUSCO_LAYOUT", planner)
+    from paper_2512_22036_b200.engine import EmulatedCluster
+
+    pkg = _pkg()
+    topo = pkg.box(1)
+    pl = pkg.round_robin_placement(E, topo)
+    a = pkg.gen_realworld(T, K, topo, pl, seed=E + K, zipf_s=zipf)
+    dev = torch.device("cuda", 0)
+    with EmulatedCluster(1, E, K, 64, T) as cl:
+        plans = cl.layout([torch.as_tensor(a.experts, device=dev)])
+        cl.check()
+        res = dict(row_of=[plans[0].row_of.cpu().numpy()], counts=[plans[0].expert_counts.cpu().numpy()],
+                   offsets=[plans[0].expert_offsets.cpu().numpy()], stats=[plans[0].stats.cpu().numpy()],
+                   first=[plans[0].first_mask.cpu().numpy()], rank_mask=[plans[0].rank_mask.cpu().numpy()],
+                   ids=[np.arange(T)])
+    _check_layout(res, a, pl, 1)
