@@ -306,8 +306,8 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
   }
   h->sms = sms;
   {
-    const char* lm = getenv("FUSCO_LAYOUT");  // cluster (default) | grid
-    h->cluster_layout = !(lm && std::string(lm) == "grid") && num_experts <= kClusterMaxE && topk <= kClusterMaxK;
+    const char* lm = getenv("FUSCO_LAYOUT");  // grid (default, measured faster) | cluster
+    h->cluster_layout = (lm && std::string(lm) == "cluster") && num_experts <= kClusterMaxE && topk <= kClusterMaxK;
     h->cluster_smem = layout_cluster_smem_bytes(num_experts, topk);
     if (h->cluster_layout) {
       e = cudaFuncSetAttribute(layout_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->cluster_smem);
@@ -323,7 +323,9 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
     const std::string cm = mode ? std::string(mode) : std::string("auto");
     const bool want_tma = cm == "tma" || (cm == "auto" && world > 1);
     h->combine_tma = (want_tma && token_bytes % 16 == 0) ? 1 : 0;
-    h->comb_sb = comb_slice_bytes(token_bytes, topk);
+    const char* cst = getenv("FUSCO_COMB_STAGE");  // bytes per stage (K row slices), default 24 KiB
+    const int stage_target = cst ? std::max(4096, std::min(96 * 1024, atoi(cst))) : kCombStageTarget;
+    h->comb_sb = comb_slice_bytes(token_bytes, topk, stage_target);
     const int stage = topk * h->comb_sb;
     const char* cctas = getenv("FUSCO_TMA_CTAS");
     const int comb_ctas = cctas ? std::max(1, std::min(8, atoi(cctas))) : 3;

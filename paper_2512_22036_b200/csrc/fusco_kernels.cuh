@@ -1008,8 +1008,8 @@ constexpr int kCombThreads = 32 * (1 + kCombConsumers);
 constexpr int kCombMaxStages = 16;
 constexpr int kCombStageTarget = 24 * 1024;  // bytes of one stage (K row slices)
 
-__host__ __device__ inline int comb_slice_bytes(int tb, int K) {
-  int sb = kCombStageTarget / K;
+__host__ __device__ inline int comb_slice_bytes(int tb, int K, int stage_target = kCombStageTarget) {
+  int sb = stage_target / K;
   sb = sb < 512 ? 512 : sb;
   if (sb >= tb) return tb;
   const int S = (tb + sb - 1) / sb;
