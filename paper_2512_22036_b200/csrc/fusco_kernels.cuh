@@ -29,11 +29,54 @@ constexpr int kMoveThreads = 256;    // dispatch / combine CTA size
 //   LOCAL : bits[8][E] + wbase[8][E]            (REMOTE aliases: tot/base/before/pre [4][E])
 //   chunk : e_s[256*K] (expert ids of the chunk) + pos_s[256*K] (in-chunk positions)
 __host__ __device__ inline size_t layout_smem_bytes(int E, int K) {
-  const size_t tables = ((size_t)E + 32) * sizeof(int32_t);
+  const size_t tables = (2ull * E + 32 + 33) * sizeof(int32_t);  // owner, perm, node, seg
   const size_t a = 2ull * kLayoutWarps * E * sizeof(uint32_t);
-  const size_t b = 4ull * E * sizeof(int32_t);
+  const size_t b = (5ull * E + 1) * sizeof(int32_t);
   const size_t chunk = 2ull * kLayoutThreads * K * sizeof(int32_t);
   return tables + (a > b ? a : b) + chunk;
+}
+
+
+// base_g(e) for every expert: exclusive scan of tot[] in (owner, expert)
+// order (perm_s), restarted at each owner's segment — one block-wide scan
+// over shared memory (no serial per-rank loop, no global loads).  ex_s gets
+// E+1 entries.  Returns nothing; rows of rank s = ex_s[seg_s[s+1]] - ex_s[seg_s[s]].
+template <int NT>
+__device__ __forceinline__ void block_segmented_base(int E, const int32_t* tot, const int32_t* perm_s,
+                                                     const int32_t* seg_s, const int32_t* owner_s,
+                                                     int32_t* ex_s, int32_t* base, int* warp_tot) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (E + NT - 1) / NT;  // consecutive elements per thread
+  const int j0 = tid * per;
+  int loc = 0;
+  for (int q = 0; q < per; ++q) {
+    const int j = j0 + q;
+    if (j < E) loc += tot[perm_s[j]];
+  }
+  const int incl = warp_incl_scan(loc, lane);
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int v = lane < NW ? warp_tot[lane] : 0;
+    const int wi = warp_incl_scan(v, lane);
+    if (lane < NW) warp_tot[lane] = wi - v;  // exclusive warp offsets
+  }
+  __syncthreads();
+  int run = warp_tot[warp] + incl - loc;
+  for (int q = 0; q < per; ++q) {
+    const int j = j0 + q;
+    if (j < E) {
+      ex_s[j] = run;
+      run += tot[perm_s[j]];
+    }
+  }
+  if (tid == NT - 1) ex_s[E] = run;  // the last thread's running sum is the grand total
+  __syncthreads();
+  for (int j = tid; j < E; j += NT) {
+    const int e = perm_s[j];
+    base[e] = ex_s[j] - ex_s[seg_s[owner_s[e]]];
+  }
 }
 
 // ===========================================================================
@@ -71,10 +114,13 @@ __global__ void __launch_bounds__(kLayoutThreads)
   const int parity = (int)(epoch & 1u);
   trace_stamp(a, FS_TRACE_LAYOUT_BEGIN);
 
+  __shared__ int warp_tot[kLayoutWarps];
   int32_t* owner_s = reinterpret_cast<int32_t*>(sm);
   int32_t* node_s = owner_s + E;
-  uint32_t* work = reinterpret_cast<uint32_t*>(node_s + 32);
-  const size_t work_words = (size_t)(2 * kLayoutWarps * E > 4 * E ? 2 * kLayoutWarps * E : 4 * E);
+  int32_t* perm_s = node_s + 32;
+  int32_t* seg_s = perm_s + E;        // [33]
+  uint32_t* work = reinterpret_cast<uint32_t*>(seg_s + 33);
+  const size_t work_words = (size_t)(2 * kLayoutWarps * E > 5 * E + 1 ? 2 * kLayoutWarps * E : 5 * E + 1);
   int32_t* e_s = reinterpret_cast<int32_t*>(work + work_words);
   int32_t* pos_s = e_s + kLayoutThreads * K;
   int32_t* totals = a.totals + (size_t)parity * E;
@@ -85,8 +131,12 @@ __global__ void __launch_bounds__(kLayoutThreads)
 
   // stage the expert table and this CTA's first chunk of indices together
   // (one memory round trip instead of two)
-  for (int e = tid; e < E; e += kLayoutThreads) owner_s[e] = a.owner[e];
+  for (int e = tid; e < E; e += kLayoutThreads) {
+    owner_s[e] = a.owner[e];
+    perm_s[e] = a.perm[e];
+  }
   if (tid < P) node_s[tid] = a.node_of[tid];
+  if (tid <= P) seg_s[tid] = a.seg_begin[tid];
   auto stage_chunk = [&](int c) {
     const int t0 = c * kLayoutThreads;
     const int nel = min(kLayoutThreads, T - t0) * K;
@@ -252,20 +302,10 @@ __global__ void __launch_bounds__(kLayoutThreads)
       }
     }
     __syncthreads();
-    // base_g(e): exclusive scan of totals over rank g's experts (one warp per rank)
-    for (int g = warp; g < P; g += kLayoutWarps) {
-      int run = 0;
-      const int jb = a.seg_begin[g], je = a.seg_begin[g + 1];
-      for (int j0 = jb; j0 < je; j0 += 32) {
-        const int j = j0 + lane;
-        const int e = j < je ? a.perm[j] : -1;
-        const int val = e >= 0 ? tot[e] : 0;
-        const int incl = warp_incl_scan(val, lane);
-        if (e >= 0) base[e] = run + incl - val;
-        run += __shfl_sync(kFull, incl, 31);
-      }
-      if (g == s && lane == 0) rows_total = run;
-    }
+    // base_g(e): exclusive scan of totals over rank g's experts
+    int32_t* ex_s = pre + E;  // [E+1]
+    block_segmented_base<kLayoutThreads>(E, tot, perm_s, seg_s, owner_s, ex_s, base, warp_tot);
+    if (tid == 0) rows_total = ex_s[seg_s[s + 1]] - ex_s[seg_s[s]];
     __syncthreads();
     for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
       if (c != c_first) {  // later chunks of this CTA (T > grid * 256)
@@ -291,9 +331,9 @@ __global__ void __launch_bounds__(kLayoutThreads)
       }
     }
     if (blockIdx.x == 0) {
-      const int jb = a.seg_begin[s], je = a.seg_begin[s + 1];
+      const int jb = seg_s[s], je = seg_s[s + 1];
       for (int j = jb + tid; j < je; j += kLayoutThreads) {
-        const int e = a.perm[j];
+        const int e = perm_s[j];
         if (expert_counts) expert_counts[j - jb] = tot[e];
         if (expert_offsets) expert_offsets[j - jb] = base[e];
       }
@@ -327,7 +367,7 @@ constexpr int kClusterMaxK = 8;
 
 __host__ __device__ inline size_t layout_cluster_smem_bytes(int E, int K) {
   // owner[E] node[32] bits[32][E] wbase[32][E] e_s[1024K] pos_s[1024K] cnt[E] tot/base/before/pre[4E]
-  return sizeof(int32_t) * ((size_t)E + 32 + 2ull * kClusterWarps * E + 2ull * kClusterThreads * K + 5ull * E);
+  return sizeof(int32_t) * (2ull * E + 32 + 33 + 2ull * kClusterWarps * E + 2ull * kClusterThreads * K + 6ull * E + 1);
 }
 
 __global__ void __launch_bounds__(kClusterThreads, 1)
@@ -348,9 +388,12 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   const int parity = (int)(epoch & 1u);
   trace_stamp(a, FS_TRACE_LAYOUT_BEGIN);
 
+  __shared__ int warp_tot[kClusterWarps];
   int32_t* owner_s = reinterpret_cast<int32_t*>(sm);
   int32_t* node_s = owner_s + E;
-  uint32_t* bits = reinterpret_cast<uint32_t*>(node_s + 32);   // [32][E]
+  int32_t* perm_s = node_s + 32;
+  int32_t* seg_s = perm_s + E;  // [33]
+  uint32_t* bits = reinterpret_cast<uint32_t*>(seg_s + 33);     // [32][E]
   uint32_t* wbase = bits + kClusterWarps * E;                   // [32][E]
   int32_t* e_s = reinterpret_cast<int32_t*>(wbase + kClusterWarps * E);
   int32_t* pos_s = e_s + kClusterThreads * K;
@@ -359,14 +402,19 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   int32_t* base = tot + E;
   int32_t* before = base + E;
   int32_t* pre = before + E;
+  int32_t* ex_s = pre + E;  // [E+1]
 
   const int t0 = (int)crank * kClusterThreads;
   const int ntok = max(0, min(kClusterThreads, T - t0));
   const int nel = ntok * K;
   const size_t base_el = (size_t)t0 * K;
   // one round trip: expert table, node table and this CTA's indices together
-  for (int e = tid; e < E; e += kClusterThreads) owner_s[e] = a.owner[e];
+  for (int e = tid; e < E; e += kClusterThreads) {
+    owner_s[e] = a.owner[e];
+    perm_s[e] = a.perm[e];
+  }
   if (tid < P) node_s[tid] = a.node_of[tid];
+  if (tid <= P) seg_s[tid] = a.seg_begin[tid];
   for (int j = tid; j < nel; j += kClusterThreads) {
     long long e = load_idx(idx, base_el + j, a.idx64);
     if (e < 0 || e >= E) {
@@ -501,19 +549,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     for (int e = tid; e < E; e += kClusterThreads) before[e] = 0;
   }
   __syncthreads();
-  for (int g = warp; g < P; g += kClusterWarps) {
-    int run = 0;
-    const int jb = a.seg_begin[g], je = a.seg_begin[g + 1];
-    for (int j0 = jb; j0 < je; j0 += 32) {
-      const int j = j0 + lane;
-      const int e = j < je ? a.perm[j] : -1;
-      const int val = e >= 0 ? tot[e] : 0;
-      const int incl = warp_incl_scan(val, lane);
-      if (e >= 0) base[e] = run + incl - val;
-      run += __shfl_sync(kFull, incl, 31);
-    }
-    if (g == s && lane == 0) rows_total = run;
-  }
+  block_segmented_base<kClusterThreads>(E, tot, perm_s, seg_s, owner_s, ex_s, base, warp_tot);
+  if (tid == 0) rows_total = ex_s[seg_s[s + 1]] - ex_s[seg_s[s]];
   __syncthreads();
   for (int e = tid; e < E; e += kClusterThreads) pre[e] += base[e] + before[e];
   __syncthreads();
@@ -523,9 +560,9 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     row_of[base_el + j] = (int32_t)r;
   }
   if (crank == 0) {
-    const int jb = a.seg_begin[s], je = a.seg_begin[s + 1];
+    const int jb = seg_s[s], je = seg_s[s + 1];
     for (int j = jb + tid; j < je; j += kClusterThreads) {
-      const int e = a.perm[j];
+      const int e = perm_s[j];
       if (expert_counts) expert_counts[j - jb] = tot[e];
       if (expert_offsets) expert_offsets[j - jb] = base[e];
     }
