@@ -29,7 +29,7 @@ constexpr int kMoveThreads = 256;    // dispatch / combine CTA size
 //   LOCAL : bits[8][E] + wbase[8][E]            (REMOTE aliases: tot/base/before/pre [4][E])
 //   chunk : e_s[256*K] (expert ids of the chunk) + pos_s[256*K] (in-chunk positions)
 __host__ __device__ inline size_t layout_smem_bytes(int E, int K) {
-  const size_t tables = (2ull * E + 32 + 33) * sizeof(int32_t);  // owner, perm, node, seg
+  const size_t tables = (3ull * E + 32 + 33) * sizeof(int32_t);  // owner, perm, node, seg, cnt
   const size_t a = 2ull * kLayoutWarps * E * sizeof(uint32_t);
   const size_t b = (5ull * E + 1) * sizeof(int32_t);
   const size_t chunk = 2ull * kLayoutThreads * K * sizeof(int32_t);
@@ -119,8 +119,11 @@ __global__ void __launch_bounds__(kLayoutThreads)
   int32_t* node_s = owner_s + E;
   int32_t* perm_s = node_s + 32;
   int32_t* seg_s = perm_s + E;        // [33]
-  uint32_t* work = reinterpret_cast<uint32_t*>(seg_s + 33);
+  int32_t* cnt_s = seg_s + 33;        // [E] this CTA's last chunk counts
+  uint32_t* work = reinterpret_cast<uint32_t*>(cnt_s + E);
   const size_t work_words = (size_t)(2 * kLayoutWarps * E > 5 * E + 1 ? 2 * kLayoutWarps * E : 5 * E + 1);
+  // a single CTA owning the only chunk needs no grid barrier and already holds the totals
+  const bool single = gridDim.x == 1 && nchunks <= 1;
   int32_t* e_s = reinterpret_cast<int32_t*>(work + work_words);
   int32_t* pos_s = e_s + kLayoutThreads * K;
   int32_t* totals = a.totals + (size_t)parity * E;
@@ -198,6 +201,7 @@ __global__ void __launch_bounds__(kLayoutThreads)
           run += __popc(bits[w * E + e]);
         }
         a.chunk_cnt[(size_t)c * E + e] = (int32_t)run;
+        cnt_s[e] = (int32_t)run;
         if (run) atomicAdd(&totals[e], (int)run);
       }
       __syncthreads();
@@ -226,7 +230,8 @@ __global__ void __launch_bounds__(kLayoutThreads)
       if (acc) atomicAdd(reinterpret_cast<unsigned long long*>(stat_acc + tid), (unsigned long long)acc);
     }
     trace_stamp(a, FS_TRACE_LAYOUT_HIST);
-    grid.sync();
+    if (single) __syncthreads();
+    else grid.sync();
     trace_stamp(a, FS_TRACE_LAYOUT_GRIDSYNC);
 
     // One CTA publishes this rank's per-expert totals into every peer's count
@@ -237,7 +242,7 @@ __global__ void __launch_bounds__(kLayoutThreads)
       long long* next_stats = a.stat_part + (parity ^ 1) * 8;
       if (P > 1) {
         for (int e = tid; e < E; e += kLayoutThreads) {
-          const int tot = ld_cg(totals + e);
+          const int tot = single ? cnt_s[e] : ld_cg(totals + e);
           for (int g = 0; g < P; ++g) {
             int32_t* dst = reinterpret_cast<int32_t*>(a.peer[g] + a.off_count + (size_t)parity * a.count_stride);
             dst[(size_t)s * E + e] = tot;
@@ -296,8 +301,9 @@ __global__ void __launch_bounds__(kLayoutThreads)
         before[e] = b;
       }
     } else {
+      const bool from_smem = single && (phase & FS_PHASE_LOCAL);
       for (int e = tid; e < E; e += kLayoutThreads) {
-        tot[e] = ld_cg(totals + e);
+        tot[e] = from_smem ? cnt_s[e] : ld_cg(totals + e);
         before[e] = 0;
       }
     }
