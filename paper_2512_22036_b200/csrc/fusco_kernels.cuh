@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(kLayoutThreads)
   for (int e = tid; e < E; e += kLayoutThreads) {
     owner_s[e] = a.owner[e];
     perm_s[e] = a.perm[e];
+    cnt_s[e] = 0;  // a rank without tokens publishes zero counts
   }
   if (tid < P) node_s[tid] = a.node_of[tid];
   if (tid <= P) seg_s[tid] = a.seg_begin[tid];
