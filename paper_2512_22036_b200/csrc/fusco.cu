@@ -63,6 +63,7 @@ struct fs_ctx {
   int tma_slots;        // smem ring slots per CTA of the TMA engine
   int tma_lag, tma_ctas;
   size_t tma_smem;
+  int comb_minb4;       // warp combine, K <= 2: force 4 CTAs/SM (FUSCO_COMB_MINB4=1)
   int cluster_layout;   // 1: single-cluster DSMEM planner usable (E <= 256, K <= 8)
   size_t cluster_smem;
   int combine_tma;      // 1: TMA combine engine (FUSCO_COMBINE=tma)
@@ -306,6 +307,8 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
   }
   h->sms = sms;
   {
+    const char* mb = getenv("FUSCO_COMB_MINB4");
+    h->comb_minb4 = mb && std::string(mb) == "1";
     const char* lm = getenv("FUSCO_LAYOUT");  // grid (default, measured faster) | cluster
     h->cluster_layout = (lm && std::string(lm) == "cluster") && num_experts <= kClusterMaxE && topk <= kClusterMaxK;
     h->cluster_smem = layout_cluster_smem_bytes(num_experts, topk);
@@ -539,7 +542,10 @@ int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes, const int32_t
   }
   // rows in flight per unit: min(K, 4) (no registers reserved for loads that never issue)
   if (vec16) {
-    if (h->K <= 2)
+    if (h->K <= 2 && h->comb_minb4)
+      fn = bf ? (f64 ? (const void*)combine_kernel<int4, true, true, 4, 2, 4> : (const void*)combine_kernel<int4, true, false, 4, 2, 4>)
+              : (f64 ? (const void*)combine_kernel<int4, false, true, 4, 2, 4> : (const void*)combine_kernel<int4, false, false, 4, 2, 4>);
+    else if (h->K <= 2)
       fn = bf ? (f64 ? (const void*)combine_kernel<int4, true, true, 4, 2> : (const void*)combine_kernel<int4, true, false, 4, 2>)
               : (f64 ? (const void*)combine_kernel<int4, false, true, 4, 2> : (const void*)combine_kernel<int4, false, false, 4, 2>);
     else
