@@ -64,6 +64,7 @@ struct fs_ctx {
   int tma_lag, tma_ctas;
   size_t tma_smem;
   int comb_minb4;       // warp combine, K <= 2: force 4 CTAs/SM (FUSCO_COMB_MINB4=1)
+  int comb_nopipe;      // K <= 2: plain warp combine instead of the pipelined one (FUSCO_COMB_NOPIPE=1)
   int cluster_layout;   // 1: single-cluster DSMEM planner usable (E <= 256, K <= 8)
   size_t cluster_smem;
   int combine_tma;      // 1: TMA combine engine (FUSCO_COMBINE=tma)
@@ -309,6 +310,8 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
   {
     const char* mb = getenv("FUSCO_COMB_MINB4");
     h->comb_minb4 = mb && std::string(mb) == "1";
+    const char* np = getenv("FUSCO_COMB_NOPIPE");
+    h->comb_nopipe = np && std::string(np) == "1";
     const char* lm = getenv("FUSCO_LAYOUT");  // grid (default, measured faster) | cluster
     h->cluster_layout = (lm && std::string(lm) == "cluster") && num_experts <= kClusterMaxE && topk <= kClusterMaxK;
     h->cluster_smem = layout_cluster_smem_bytes(num_experts, topk);
@@ -541,7 +544,10 @@ int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes, const int32_t
     return FS_OK;
   }
   // rows in flight per unit: min(K, 4) (no registers reserved for loads that never issue)
-  if (vec16) {
+  if (vec16 && h->K <= 2 && !h->comb_minb4 && !h->comb_nopipe) {
+    fn = bf ? (f64 ? (const void*)combine_k2_kernel<true, true> : (const void*)combine_k2_kernel<true, false>)
+            : (f64 ? (const void*)combine_k2_kernel<false, true> : (const void*)combine_k2_kernel<false, false>);
+  } else if (vec16) {
     if (h->K <= 2 && h->comb_minb4)
       fn = bf ? (f64 ? (const void*)combine_kernel<int4, true, true, 4, 2, 4> : (const void*)combine_kernel<int4, true, false, 4, 2, 4>)
               : (f64 ? (const void*)combine_kernel<int4, false, true, 4, 2, 4> : (const void*)combine_kernel<int4, false, false, 4, 2, 4>);

@@ -1036,6 +1036,159 @@ __global__ void __launch_bounds__(kMoveThreads, MINB)
 }
 
 // ===========================================================================
+// Combine, software-pipelined warp engine for K <= 2 (Mixtral-like top-2)
+//
+// Same math and order as combine_kernel, but each warp keeps two units in
+// flight: the row loads of unit n+1 are issued before unit n is reduced and
+// stored, and the (expert, row) metadata is prefetched two units ahead, so a
+// warp's memory parallelism doubles without more warps.
+// ===========================================================================
+template <bool BF16, bool ACC64>
+__global__ void __launch_bounds__(kMoveThreads)
+    combine_k2_kernel(FsArgs a, const void* __restrict__ idx, const int32_t* __restrict__ row_of,
+                      const void* __restrict__ topk_w, int w64, int4* __restrict__ out, int src_sel, int phase) {
+  using Acc = typename std::conditional<ACC64, double, float>::type;
+  using EL = Elem<int4, BF16>;
+  constexpr int U = 4;
+  constexpr int SW = 32 * U;
+  const int K = a.K, T = a.T, P = a.world, s = a.rank;
+  const int nv = a.tb / 16;
+  const int S = (nv + SW - 1) / SW;
+  const int lane = threadIdx.x & 31;
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  const uint32_t epoch = load_epoch(a);
+  const size_t src_off =
+      src_sel == FS_SRC_ACT_OUT ? a.off_actout : a.off_act + (size_t)(epoch & 1u) * a.act_stride;
+  trace_stamp(a, FS_TRACE_COMBINE_BEGIN);
+  if ((phase & FS_PHASE_LOCAL) && P > 1) {
+    if (blockIdx.x == 0 && threadIdx.x < P)
+      st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[threadIdx.x] + kOffReadyFlag) + s, epoch);
+  }
+  if (!(phase & FS_PHASE_REMOTE)) return;
+  if (P > 1) {
+    if (threadIdx.x < P)
+      wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffReadyFlag) + threadIdx.x, epoch, a);
+    __syncthreads();
+  }
+  trace_stamp(a, FS_TRACE_COMBINE_READY);
+  __shared__ int32_t owner_sm[kMaxExperts];
+  load_owner_table(a, owner_sm);
+  const long long units = (long long)T * S;
+
+  struct Unit {
+    long long u;
+    const int4* src[2];
+    Acc w[2];
+    int w0, rem;
+  };
+  auto load_w = [&](long long uu) -> Acc {
+    if (lane >= K) return (Acc)0;
+    const size_t pos = (size_t)(uu / S) * K + lane;
+    return w64 ? (Acc)reinterpret_cast<const double*>(topk_w)[pos]
+               : (Acc)reinterpret_cast<const float*>(topk_w)[pos];
+  };
+  // metadata (lanes 0..K-1) -> per-unit row pointers, broadcast to the warp
+  auto resolve = [&](long long uu, const KMeta& m, Acc wl) -> Unit {
+    Unit x;
+    x.u = uu;
+    const int i = (int)(uu / S), sl = (int)(uu - (long long)i * S);
+    x.w0 = sl * SW;
+    x.rem = nv - x.w0;
+    int g = 0, r = 0;
+    if (lane < K) {
+      g = owner_sm[m.e];
+      r = (m.r < 0 || m.r >= a.max_rows) ? 0 : m.r;
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int gk = __shfl_sync(kFull, g, k);
+      const int rk = __shfl_sync(kFull, r, k);
+      x.w[k] = __shfl_sync(kFull, wl, k);
+      x.src[k] = reinterpret_cast<const int4*>(a.peer[gk] + src_off) + (size_t)rk * nv + x.w0;
+    }
+    (void)i;
+    return x;
+  };
+  auto issue = [&](const Unit& x, int4 (&v)[2][U]) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int w = j * 32 + lane;
+        if (k < K && w < x.rem) v[k][j] = ld_nc(x.src[k] + w);
+      }
+  };
+  auto finish = [&](const Unit& x, const int4 (&v)[2][U]) {
+    const int i = (int)(x.u / S);
+    int4* dst = out + (size_t)i * nv + x.w0;
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int w = j * 32 + lane;
+      if (w < x.rem) {
+        Acc acc[EL::N];
+#pragma unroll
+        for (int q = 0; q < EL::N; ++q) acc[q] = (Acc)0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+          if (k < K)
+#pragma unroll
+            for (int q = 0; q < EL::N; ++q) acc[q] = fma_acc<Acc>(x.w[k], EL::get(v[k][j], q), acc[q]);
+        int4 o;
+#pragma unroll
+        for (int q = 0; q < EL::kWords; ++q) {
+          if constexpr (BF16) set_word(o, q, pack_out(acc[2 * q], acc[2 * q + 1]));
+          else set_word(o, q, f32_bits(acc[q]));
+        }
+        st_na(dst + w, o);
+      }
+    }
+  };
+
+  long long u = gw;
+  if (u >= units) return;
+  KMeta m_next = load_meta(a, idx, row_of, (int)(u / S), lane);
+  Acc w_next = load_w(u);
+  Unit cur = resolve(u, m_next, w_next);
+  if (u + nw < units) {
+    m_next = load_meta(a, idx, row_of, (int)((u + nw) / S), lane);
+    w_next = load_w(u + nw);
+  }
+  int4 va[2][U], vb[2][U];
+  issue(cur, va);
+  for (;;) {
+    // ---- cur in va; next goes to vb
+    const long long u1 = cur.u + nw;
+    Unit nxt;
+    if (u1 < units) {
+      nxt = resolve(u1, m_next, w_next);
+      if (u1 + nw < units) {
+        m_next = load_meta(a, idx, row_of, (int)((u1 + nw) / S), lane);
+        w_next = load_w(u1 + nw);
+      }
+      issue(nxt, vb);
+    }
+    finish(cur, va);
+    if (u1 >= units) break;
+    cur = nxt;
+    // ---- cur in vb; next goes to va
+    const long long u2 = cur.u + nw;
+    if (u2 < units) {
+      nxt = resolve(u2, m_next, w_next);
+      if (u2 + nw < units) {
+        m_next = load_meta(a, idx, row_of, (int)((u2 + nw) / S), lane);
+        w_next = load_w(u2 + nw);
+      }
+      issue(nxt, va);
+    }
+    finish(cur, vb);
+    if (u2 >= units) break;
+    cur = nxt;
+  }
+  trace_stamp(a, FS_TRACE_COMBINE_END);
+}
+
+// ===========================================================================
 // Combine, TMA engine
 //
 // Work item = (token i, column slice j of SB bytes).  Warp 0 resolves the
