@@ -82,6 +82,7 @@ struct fs_ctx {
   int* status_d;
   int* num_rows_d;
   uint32_t* epoch_d;  // device iteration counter (graph-replay safe)
+  unsigned long long* work_d;  // [2][8] dynamic work counters
   unsigned long long* trace_d;  // FS_NTRACE stamps when FUSCO_TRACE=1, else null
 };
 
@@ -118,6 +119,7 @@ FsArgs make_args(const fs_ctx* h, int T, int idx64) {
   a.num_rows = h->num_rows_d;
   a.timeout_ns = h->timeout_ns;
   a.trace = h->trace_d;
+  a.work = h->work_d;
   return a;
 }
 
@@ -367,7 +369,8 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
       (e = dalloc((void**)&h->stat_part_d, (size_t)2 * 8 * 8)) != cudaSuccess ||
       (e = dalloc((void**)&h->status_d, 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->num_rows_d, 4)) != cudaSuccess ||
-      (e = dalloc((void**)&h->epoch_d, 4)) != cudaSuccess)
+      (e = dalloc((void**)&h->epoch_d, 4)) != cudaSuccess ||
+      (e = dalloc((void**)&h->work_d, 2 * 8 * 8)) != cudaSuccess)
     return cleanup(fail(FS_ECUDA, std::string("fs_create alloc: ") + cudaGetErrorString(e)));
   if ((e = cudaMemcpy(h->owner_d, owner.data(), num_experts * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(h->node_of_d, nodes.data(), world * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
@@ -376,6 +379,7 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
       (e = cudaMemset(h->status_d, 0, 4)) != cudaSuccess ||
       (e = cudaMemset(h->num_rows_d, 0, 4)) != cudaSuccess ||
       (e = cudaMemset(h->epoch_d, 0, 4)) != cudaSuccess ||
+      (e = cudaMemset(h->work_d, 0, 2 * 8 * 8)) != cudaSuccess ||
       (e = cudaMemset(h->totals_d, 0, (size_t)2 * num_experts * 4)) != cudaSuccess ||
       (e = cudaMemset(h->stat_part_d, 0, (size_t)2 * 8 * 8)) != cudaSuccess ||
       (e = cudaDeviceSynchronize()) != cudaSuccess)
@@ -405,6 +409,7 @@ int fs_destroy(fs_handle_t h) {
   cudaFree(h->status_d);
   cudaFree(h->num_rows_d);
   cudaFree(h->epoch_d);
+  cudaFree(h->work_d);
   if (h->trace_d) cudaFree(h->trace_d);
   delete h;
   return FS_OK;

@@ -50,7 +50,13 @@ struct FsArgs {
   int* num_rows;             // rows of the own activation buffer this epoch
   unsigned long long timeout_ns;
   unsigned long long* trace;  // optional globaltimer stamps (FUSCO_TRACE=1), see FS_TRACE_*
+  unsigned long long* work;   // [2][8] per-parity dynamic work counters (zeroed one epoch ahead)
 };
+
+// dynamic work counters (slot within work[parity][*])
+constexpr int kWorkDispatch = 0;
+constexpr int kWorkFanout = 1;
+constexpr int kWorkCombine = 2;
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -187,6 +193,17 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
     if (lane >= o) v += n;
   }
   return v;
+}
+
+// One lane claims the next work unit for the warp (dynamic load balancing:
+// warps that drew light units simply claim more).
+__device__ __forceinline__ long long claim_warp(unsigned long long* ctr) {
+  unsigned long long v = 0;
+  if ((threadIdx.x & 31) == 0) v = atomicAdd(ctr, 1ull);
+  return (long long)__shfl_sync(0xffffffffu, v, 0);
+}
+__device__ __forceinline__ unsigned long long* work_ctr(const FsArgs& a, uint32_t epoch, int slot) {
+  return a.work + (size_t)(epoch & 1u) * 8 + slot;
 }
 
 __device__ __forceinline__ uint32_t load_epoch(const FsArgs& a) {

@@ -256,7 +256,10 @@ __global__ void __launch_bounds__(kLayoutThreads)
         stats[slot[tid]] = *reinterpret_cast<volatile long long*>(stat_acc + tid);
       }
       if (stats && tid >= 5 && tid < FS_NSTATS) stats[tid] = 0;
-      if (tid < 8) next_stats[tid] = 0;
+      if (tid < 8) {
+        next_stats[tid] = 0;
+        a.work[(size_t)(parity ^ 1) * 8 + tid] = 0ull;  // the next epoch's work counters
+      }
       // every CTA read the old epoch before the grid barrier: safe to bump
       if (tid == 0) *a.epoch_ptr = epoch;
       if (P > 1) {
@@ -526,6 +529,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
       stats[slot[tid]] = acc;
     }
     if (stats && tid >= 5 && tid < FS_NSTATS) stats[tid] = 0;
+    if (tid < 8) a.work[(size_t)(parity ^ 1) * 8 + tid] = 0ull;
     if (tid == 0) *a.epoch_ptr = epoch;  // every CTA read the old epoch before the cluster barrier
     if (P > 1) {
       __syncthreads();
@@ -663,6 +667,7 @@ __device__ __forceinline__ void fan_out_rows(const FsArgs& a, size_t act_off, si
   const int32_t* fs = reinterpret_cast<const int32_t*>(a.peer[a.rank] + fan_off);
   V* act = reinterpret_cast<V*>(a.peer[a.rank] + act_off);
   const long long units = (long long)rows * S;
+  // static striding: most units are no-ops (f == r), a claim per unit would cost more than it balances
   for (long long u = gw; u < units; u += nw) {
     const int r = (int)(u / S), sl = (int)(u - (long long)r * S);
     const int f = ld_cg(fs + r);
@@ -702,13 +707,15 @@ __global__ void __launch_bounds__(kMoveThreads)
     __shared__ int32_t owner_sm[kMaxExperts];
     load_owner_table(a, owner_sm);
     const long long units = (long long)T * S;
-    long long u = gw;
+    unsigned long long* ctr = work_ctr(a, epoch, kWorkDispatch);
+    long long u = claim_warp(ctr);
     KMeta nxt = u < units ? load_meta(a, idx, row_of, (int)(u / S), lane) : KMeta{0, -1};
-    for (; u < units; u += nw) {
+    while (u < units) {
       const int i = (int)(u / S);
       const int sl = (int)(u - (long long)i * S);
       const KMeta cur = nxt;
-      if (u + nw < units) nxt = load_meta(a, idx, row_of, (int)((u + nw) / S), lane);
+      const long long un = claim_warp(ctr);  // next unit: claimed and prefetched during this one
+      if (un < units) nxt = load_meta(a, idx, row_of, (int)(un / S), lane);
       // payload loads first: they do not depend on the destinations
       const int w0 = sl * SW;
       const V* src = x + (size_t)i * nv + w0;
@@ -751,6 +758,7 @@ __global__ void __launch_bounds__(kMoveThreads)
           if (w < rem) st_na(dst + w, v[j]);
         }
       }
+      u = un;
     }
     if (P > 1) signal_pushed(a, epoch);
   }
@@ -1221,7 +1229,11 @@ __global__ void __launch_bounds__(kCombThreads)
   using Acc = typename std::conditional<ACC64, double, float>::type;
   using EL = Elem<int4, BF16>;
   extern __shared__ __align__(128) char csm[];
-  __shared__ Acc w_s[kCombConsumers][32];
+  // per stage: the claimed item (-1 = no more work) and its K weights, written
+  // by the producer before it arms the stage's full barrier
+  __shared__ long long slot_item[kCombMaxStages];
+  __shared__ Acc slot_w[kCombMaxStages][32];
+  __shared__ int32_t owner_cmb[kMaxExperts];
   uint64_t* full = reinterpret_cast<uint64_t*>(csm);
   uint64_t* empty = full + kCombMaxStages;
   char* stages = csm + 2 * kCombMaxStages * sizeof(uint64_t);
@@ -1239,7 +1251,6 @@ __global__ void __launch_bounds__(kCombThreads)
       st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[threadIdx.x] + kOffReadyFlag) + s, epoch);
   }
   if (!(phase & FS_PHASE_REMOTE)) return;
-  __shared__ int32_t owner_cmb[kMaxExperts];
   for (int e = threadIdx.x; e < a.E; e += blockDim.x) owner_cmb[e] = a.owner[e];
   if (threadIdx.x == 0) {
     for (int q = 0; q < nstages; ++q) {
@@ -1254,62 +1265,73 @@ __global__ void __launch_bounds__(kCombThreads)
   trace_stamp(a, FS_TRACE_COMBINE_READY);
   const long long items = (long long)T * S;
 
-  if (warp == 0) {  // producer
-    int cur_tok = -1, g = 0, r = 0;
+  if (warp == 0) {  // producer: claims items dynamically, one ahead (metadata + weights prefetched)
+    unsigned long long* ctr = work_ctr(a, epoch, kWorkCombine);
+    auto load_w = [&](long long uu) -> Acc {
+      if (lane >= K) return (Acc)0;
+      const size_t pos = (size_t)(uu / S) * K + lane;
+      return w64 ? (Acc)reinterpret_cast<const double*>(topk_w)[pos]
+                 : (Acc)reinterpret_cast<const float*>(topk_w)[pos];
+    };
+    long long u = claim_warp(ctr);
+    KMeta m = u < items ? load_meta(a, idx, row_of, (int)(u / S), lane) : KMeta{0, 0};
+    Acc wl = u < items ? load_w(u) : (Acc)0;
     int n = 0;
-    long long u = blockIdx.x;
-    int nxt_tok = u < items ? (int)(u / S) : -1;
-    KMeta nxt = nxt_tok >= 0 ? load_meta(a, idx, row_of, nxt_tok, lane) : KMeta{0, 0};
-    for (; u < items; u += gridDim.x, ++n) {
-      const int i = (int)(u / S), j = (int)(u - (long long)i * S);
-      if (i != cur_tok) {
-        cur_tok = i;
-        // nxt holds token i: consume it and prefetch the CTA's next token
-        const KMeta cur = nxt;
-        long long un = u + gridDim.x;
-        while (un < items && (int)(un / S) == i) un += gridDim.x;
-        if (un < items) nxt = load_meta(a, idx, row_of, (int)(un / S), lane);
-        if (lane < K) {
-          g = owner_cmb[cur.e];
-          r = (cur.r < 0 || cur.r >= a.max_rows) ? 0 : cur.r;
-        }
-      }
+    for (;; ++n) {
       const int q = n % nstages;
       if (n >= nstages) mbar_wait(&empty[q], ((n / nstages) & 1) ^ 1);
+      if (u >= items) {  // sentinel: consumers stop at this stage
+        if (lane == 0) {
+          slot_item[q] = -1;
+          mbar_arrive(&full[q]);
+        }
+        break;
+      }
+      const long long un = claim_warp(ctr);  // claimed and prefetched while this item streams
+      KMeta mn = KMeta{0, 0};
+      Acc wn = (Acc)0;
+      if (un < items) {
+        mn = load_meta(a, idx, row_of, (int)(un / S), lane);
+        wn = load_w(un);
+      }
+      const int i = (int)(u / S), j = (int)(u - (long long)i * S);
+      (void)i;
       const int off = j * sb;
       const int len = min(sb, tb - off);
+      int g = 0, r = 0;
+      if (lane < K) {
+        g = owner_cmb[m.e];
+        r = (m.r < 0 || m.r >= a.max_rows) ? 0 : m.r;
+        slot_w[q][lane] = wl;
+      }
+      if (lane == 0) slot_item[q] = u;
+      __syncwarp();
       if (lane == 0) mbar_arrive_expect_tx(&full[q], (uint32_t)(K * len));
       __syncwarp();
       if (lane < K)
         bulk_load(stages + (size_t)q * stage_bytes + (size_t)lane * sb,
                   a.peer[g] + src_off + (size_t)r * tb + off, (uint32_t)len, &full[q]);
+      u = un;
+      m = mn;
+      wl = wn;
     }
   } else {  // consumers
     const int ct = threadIdx.x - 32;  // 0 .. 32*kCombConsumers-1
-    int n = 0;
-    auto load_w = [&](long long uu) -> Acc {
-      if (lane >= K || uu >= items) return (Acc)0;
-      const size_t pos = (size_t)(uu / S) * K + lane;
-      return w64 ? (Acc)reinterpret_cast<const double*>(topk_w)[pos]
-                 : (Acc)reinterpret_cast<const float*>(topk_w)[pos];
-    };
-    Acc w_next = load_w(blockIdx.x);
-    for (long long u = blockIdx.x; u < items; u += gridDim.x, ++n) {
-      const int i = (int)(u / S), j = (int)(u - (long long)i * S);
+    for (int n = 0;; ++n) {
       const int q = n % nstages;
+      mbar_wait(&full[q], (n / nstages) & 1);
+      const long long u = slot_item[q];
+      if (u < 0) break;
+      const int i = (int)(u / S), j = (int)(u - (long long)i * S);
       const int off = j * sb;
       const int nv = min(sb, tb - off) / 16;
-      if (lane < K) w_s[warp - 1][lane] = w_next;
-      w_next = load_w(u + gridDim.x);  // in flight while this item is reduced
-      __syncwarp();
-      mbar_wait(&full[q], (n / nstages) & 1);
       const char* st = stages + (size_t)q * stage_bytes;
       for (int v = ct; v < nv; v += 32 * kCombConsumers) {
         Acc acc[EL::N];
 #pragma unroll
         for (int e = 0; e < EL::N; ++e) acc[e] = (Acc)0;
         for (int k = 0; k < K; ++k) {
-          const Acc wk = w_s[warp - 1][k];
+          const Acc wk = slot_w[q][k];
           const int4 x = *reinterpret_cast<const int4*>(st + (size_t)k * sb + (size_t)v * 16);
 #pragma unroll
           for (int e = 0; e < EL::N; ++e) acc[e] = fma_acc<Acc>(wk, EL::get(x, e), acc[e]);
@@ -1322,7 +1344,7 @@ __global__ void __launch_bounds__(kCombThreads)
         }
         st_na(reinterpret_cast<int4*>(out + (size_t)i * tb + off) + v, o);
       }
-      __syncwarp();  // also orders this item's w_s reads before the next item's writes
+      __syncwarp();
       if (lane == 0) mbar_arrive(&empty[q]);
     }
   }
