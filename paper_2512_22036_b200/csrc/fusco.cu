@@ -63,6 +63,7 @@ struct fs_ctx {
   int tma_slots;        // smem ring slots per CTA of the TMA engine
   int tma_lag, tma_ctas;
   size_t tma_smem;
+  int pdl;              // 1: programmatic dependent launch planner -> dispatch (FUSCO_PDL=0 disables)
   int comb_minb4;       // warp combine, K <= 2: force 4 CTAs/SM (FUSCO_COMB_MINB4=1)
   int comb_nopipe;      // K <= 2: plain warp combine instead of the pipelined one (FUSCO_COMB_NOPIPE=1)
   int cluster_layout;   // 1: single-cluster DSMEM planner usable (E <= 256, K <= 8)
@@ -310,6 +311,8 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
   }
   h->sms = sms;
   {
+    const char* pd = getenv("FUSCO_PDL");
+    h->pdl = !(pd && std::string(pd) == "0");
     const char* mb = getenv("FUSCO_COMB_MINB4");
     h->comb_minb4 = mb && std::string(mb) == "1";
     const char* np = getenv("FUSCO_COMB_NOPIPE");
@@ -501,8 +504,27 @@ int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_byte
   if (!aligned(x, 4)) return fail(FS_EINVAL, "x must be 4-byte aligned");
   if (h->dispatch_tma && vec16) {  // unaligned x falls back to the warp mover (same grid)
     int nslots = h->tma_slots;
-    void* targs[] = {&a, (void*)&x, (void*)&topk_idx, (void*)&row_of, &phase, &nslots};
     const void* tfn = h->tma_lag == 4 ? (const void*)dispatch_tma_kernel<4> : (const void*)dispatch_tma_kernel<2>;
+    if (h->world == 1 && h->pdl) {
+      // No cross-CTA or cross-rank waits at P=1: a plain launch with PDL behind
+      // the planner, so row prefetch overlaps the planner's tail.
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(h->move_grid);
+      cfg.blockDim = dim3(kTmaThreads);
+      cfg.dynamicSmemBytes = h->tma_smem;
+      cfg.stream = (cudaStream_t)stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (h->tma_lag == 4)
+        FS_CUDA(cudaLaunchKernelEx(&cfg, dispatch_tma_kernel<4>, a, (const char*)x, topk_idx, row_of, phase, nslots));
+      else
+        FS_CUDA(cudaLaunchKernelEx(&cfg, dispatch_tma_kernel<2>, a, (const char*)x, topk_idx, row_of, phase, nslots));
+      return FS_OK;
+    }
+    void* targs[] = {&a, (void*)&x, (void*)&topk_idx, (void*)&row_of, &phase, &nslots};
     FS_CUDA(cudaLaunchCooperativeKernel(tfn, dim3(h->move_grid), dim3(kTmaThreads),
                                         targs, h->tma_smem, (cudaStream_t)stream));
     return FS_OK;
@@ -552,6 +574,24 @@ int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes, const int32_t
   if (vec16 && h->K <= 2 && !h->comb_minb4 && !h->comb_nopipe) {
     fn = bf ? (f64 ? (const void*)combine_k2_kernel<true, true> : (const void*)combine_k2_kernel<true, false>)
             : (f64 ? (const void*)combine_k2_kernel<false, true> : (const void*)combine_k2_kernel<false, false>);
+    if (h->world == 1 && h->pdl) {  // no cross-CTA waits at P=1: PDL launch behind the dispatch
+      int occ = 0;
+      if (int rc = occupancy(fn, kMoveThreads, 0, &occ)) return rc;
+      occ = std::max(1, std::min(occ, kMaxCtasPerSm));
+      int grid = occ * h->sms;
+      if (h->combine_grid_cap > 0) grid = std::min(grid, h->combine_grid_cap);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(kMoveThreads);
+      cfg.stream = (cudaStream_t)stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      FS_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+      return FS_OK;
+    }
   } else if (vec16) {
     if (h->K <= 2 && h->comb_minb4)
       fn = bf ? (f64 ? (const void*)combine_kernel<int4, true, true, 4, 2, 4> : (const void*)combine_kernel<int4, true, false, 4, 2, 4>)

@@ -270,6 +270,16 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// ---- programmatic dependent launch (PDL) ----------------------------------
+// The planner lets the next kernel on the stream start launching right away;
+// the dependent kernel does independent prologue work and then waits for the
+// planner's completion (and memory visibility) with griddepcontrol.wait.  Both
+// are no-ops for kernels launched without the PDL attribute.
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---- thread-block cluster / distributed shared memory ----------------------
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(kLayoutThreads)
   const uint32_t epoch = load_epoch(a) + ((phase & FS_PHASE_LOCAL) ? 1u : 0u);
   const int parity = (int)(epoch & 1u);
   trace_stamp(a, FS_TRACE_LAYOUT_BEGIN);
+  griddep_launch_dependents();  // the dispatch may start its row prefetch now
 
   __shared__ int warp_tot[kLayoutWarps];
   int32_t* owner_s = reinterpret_cast<int32_t*>(sm);
@@ -397,6 +398,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   const uint32_t epoch = load_epoch(a) + 1u;
   const int parity = (int)(epoch & 1u);
   trace_stamp(a, FS_TRACE_LAYOUT_BEGIN);
+  griddep_launch_dependents();
 
   __shared__ int warp_tot[kClusterWarps];
   int32_t* owner_s = reinterpret_cast<int32_t*>(sm);
@@ -804,6 +806,25 @@ __global__ void __launch_bounds__(kTmaThreads)
   const int K = a.K, T = a.T, P = a.world, s = a.rank, tb = a.tb;
   const int slot_bytes = tma_slot_bytes(tb);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ int32_t owner_tma[kMaxExperts];
+  // Prologue independent of the planner (launched with PDL behind it): barrier
+  // init, expert table, and the first ring-full of token rows streaming in.
+  if ((phase & FS_PHASE_LOCAL) && threadIdx.x == 0) {
+    for (int q = 0; q < nslots; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 1);
+    }
+    mbar_fence_init();
+  }
+  if (phase & FS_PHASE_LOCAL) load_owner_table(a, owner_tma);
+  if ((phase & FS_PHASE_LOCAL) && threadIdx.x == 0) {
+    int n = 0;
+    for (int i = blockIdx.x; i < T && n < nslots; i += gridDim.x, ++n) {
+      mbar_arrive_expect_tx(&full[n], (uint32_t)tb);
+      bulk_load(ring + (size_t)n * slot_bytes, x + (size_t)i * tb, (uint32_t)tb, &full[n]);
+    }
+  }
+  griddep_wait();  // row_of / the epoch come from the planner
   const uint32_t epoch = load_epoch(a);
   const int parity = (int)(epoch & 1u);
   const size_t act_off = a.off_act + (size_t)parity * a.act_stride;
@@ -811,21 +832,13 @@ __global__ void __launch_bounds__(kTmaThreads)
   trace_stamp(a, FS_TRACE_DISPATCH_BEGIN);
 
   if (phase & FS_PHASE_LOCAL) {
-    __shared__ int32_t owner_tma[kMaxExperts];
-    if (threadIdx.x == 0) {
-      for (int q = 0; q < nslots; ++q) {
-        mbar_init(&full[q], 1);
-        mbar_init(&empty[q], 1);
-      }
-      mbar_fence_init();
-    }
-    load_owner_table(a, owner_tma);
     if (warp == 0) {
-      if (lane == 0) {  // producer
+      if (lane == 0) {  // producer (the first nslots rows were issued in the prologue)
         int n = 0;
         for (int i = blockIdx.x; i < T; i += gridDim.x, ++n) {
+          if (n < nslots) continue;
           const int q = n % nslots;
-          if (n >= nslots) mbar_wait(&empty[q], ((n / nslots) & 1) ^ 1);
+          mbar_wait(&empty[q], ((n / nslots) & 1) ^ 1);
           mbar_arrive_expect_tx(&full[q], (uint32_t)tb);
           bulk_load(ring + (size_t)q * slot_bytes, x + (size_t)i * tb, (uint32_t)tb, &full[q]);
         }
@@ -866,6 +879,7 @@ __global__ void __launch_bounds__(kTmaThreads)
     }
     if (P > 1) signal_pushed(a, epoch);
   }
+  griddep_launch_dependents();  // the combine may start its prologue
 
   trace_stamp(a, FS_TRACE_DISPATCH_PUSHED);
   if ((phase & FS_PHASE_REMOTE) && P > 1) {
@@ -1065,6 +1079,9 @@ __global__ void __launch_bounds__(kMoveThreads)
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  __shared__ int32_t owner_sm[kMaxExperts];
+  load_owner_table(a, owner_sm);  // prologue (static table) before the PDL wait
+  griddep_wait();                 // dispatched rows / epoch from the previous kernel
   const uint32_t epoch = load_epoch(a);
   const size_t src_off =
       src_sel == FS_SRC_ACT_OUT ? a.off_actout : a.off_act + (size_t)(epoch & 1u) * a.act_stride;
@@ -1080,8 +1097,6 @@ __global__ void __launch_bounds__(kMoveThreads)
     __syncthreads();
   }
   trace_stamp(a, FS_TRACE_COMBINE_READY);
-  __shared__ int32_t owner_sm[kMaxExperts];
-  load_owner_table(a, owner_sm);
   const long long units = (long long)T * S;
 
   struct Unit {
