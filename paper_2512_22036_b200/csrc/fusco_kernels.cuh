@@ -279,15 +279,19 @@ __global__ void __launch_bounds__(kLayoutThreads)
     int32_t* before = base + E;
     int32_t* pre = before + E;
     // this CTA's chunk offsets Σ_{c'<c} cnt[c'][e] — issued before the peer
-    // wait so their latency overlaps it (only the CTA's first chunk here)
+    // wait so their latency overlaps it (only the CTA's first chunk here).
+    // All threads sweep the contiguous [c][E] prefix (coalesced, independent
+    // loads) and fold into shared memory.
     const int c_first = blockIdx.x;
-    if (c_first < nchunks)
-      for (int e = tid; e < E; e += kLayoutThreads) {
-        int acc = 0;
-#pragma unroll 8
-        for (int c2 = 0; c2 < c_first; ++c2) acc += ld_cg(a.chunk_cnt + (size_t)c2 * E + e);
-        pre[e] = acc;
+    for (int e = tid; e < E; e += kLayoutThreads) pre[e] = 0;
+    __syncthreads();
+    if (c_first < nchunks) {
+      const int nprev = c_first * E;
+      for (int j = tid; j < nprev; j += kLayoutThreads) {
+        const int v = ld_cg(a.chunk_cnt + j);
+        if (v) atomicAdd(&pre[j % E], v);
       }
+    }
     if (P > 1) {
       if (tid < P)
         wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffCountFlag) + tid, epoch, a);
@@ -321,12 +325,13 @@ __global__ void __launch_bounds__(kLayoutThreads)
     for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
       if (c != c_first) {  // later chunks of this CTA (T > grid * 256)
         __syncthreads();
-        for (int e = tid; e < E; e += kLayoutThreads) {
-          int acc = 0;
-#pragma unroll 8
-          for (int c2 = 0; c2 < c; ++c2) acc += ld_cg(a.chunk_cnt + (size_t)c2 * E + e);
-          pre[e] = acc;
+        for (int e = tid; e < E; e += kLayoutThreads) pre[e] = 0;
+        __syncthreads();
+        for (int j = tid; j < c * E; j += kLayoutThreads) {
+          const int v = ld_cg(a.chunk_cnt + j);
+          if (v) atomicAdd(&pre[j % E], v);
         }
+        __syncthreads();
       }
       for (int e = tid; e < E; e += kLayoutThreads) pre[e] += base[e] + before[e];
       __syncthreads();
