@@ -326,13 +326,27 @@ def run_exchange(
     next-row GPU baseline and are not implemented on this path yet.
     """
     ablate = _validate(assignment, topo, placement, token_bytes, mode, ablate)
-    if ablate & {"planner", "dcomm"}:
-        raise NotImplementedError("planner/dcomm ablations (GPU disaggregated baseline) are not built yet")
     tdt, code = dtype_code(dtype)
     if acc not in _ACCS:
         raise ValueError("acc must be 'f32' or 'f64'")
+    if "dcomm" in ablate:
+        return _run_disaggregated(assignment, topo, placement, token_bytes, payload_seed=payload_seed,
+                                  balancer=balancer, mode=mode, expert_fn=expert_fn, materialize=materialize,
+                                  dtype=dtype, acc=acc, device=device)
     identity = expert_fn is identity_expert
-    sess = _Session(assignment, topo, placement, token_bytes, with_act_out=not identity, device=device)
+    import os
+
+    prev = os.environ.get("FUSCO_NODEDUP")
+    if "planner" in ablate:  # no dedup: every (token, k) row crosses the link
+        os.environ["FUSCO_NODEDUP"] = "1"
+    try:
+        sess = _Session(assignment, topo, placement, token_bytes, with_act_out=not identity, device=device)
+    finally:
+        if "planner" in ablate:
+            if prev is None:
+                os.environ.pop("FUSCO_NODEDUP", None)
+            else:
+                os.environ["FUSCO_NODEDUP"] = prev
     try:
         cl, P, dev = sess.cluster, sess.P, sess.dev
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
@@ -375,6 +389,11 @@ def run_exchange(
         t_plan = ev[0].elapsed_time(ev[1]) * 1e-3
         t_disp = ev[2].elapsed_time(ev[3]) * 1e-3
         t_comb = ev[4].elapsed_time(ev[5]) * 1e-3
+        if "planner" in ablate:
+            d.inter_bytes_total = naive_inter_node_bytes(assignment, placement, topo, token_bytes)
+            d.groups = None
+            c.groups = None
+            groups = None
         drep = PhaseReport("dispatch", mode, t_plan, 0.0, t_disp, d.inter_bytes_total, d.intra_bytes_total,
                            d.intra_gpu_bytes, 0)
         crep = PhaseReport("combine", mode, 0.0, 0.0, t_comb, c.inter_bytes_total, c.intra_bytes_total,
@@ -383,6 +402,45 @@ def run_exchange(
                               buffers)
     finally:
         sess.close()
+
+
+def _run_disaggregated(assignment, topo, placement, token_bytes, *, payload_seed, balancer, mode, expert_fn,
+                       materialize, dtype, acc, device):
+    """ablate={"dcomm"}: the disaggregated pack / all-to-all / unpack shuffle
+    (reference run_baseline, engine.py:552-625) with the same output bytes;
+    rearrange bytes = 4 passes (engine.py:628-630)."""
+    from .baseline import emulated_exchange
+
+    tdt, _ = dtype_code(dtype)
+    sess = _Session(assignment, topo, placement, token_bytes, with_act_out=False, device=device)
+    try:
+        plans = sess.plans()  # layouts / counters for the host plan objects
+        sess.cluster.check()
+        d = sess.host_plan(plans, "dispatch", None)
+        c = sess.host_plan(plans, "combine", None)
+    finally:
+        sess.close()
+    dev = sess.dev
+    payloads = make_token_payloads(assignment.num_tokens, token_bytes, payload_seed)
+    xs = [torch.as_tensor(payloads[i], device=dev).contiguous().view(tdt) for i in sess.ids]
+    idxs = [torch.as_tensor(assignment.experts[i], device=dev) for i in sess.ids]
+    ws = [torch.as_tensor(assignment.weights[i], dtype=torch.float64, device=dev) for i in sess.ids]
+    fn = None if expert_fn is identity_expert else expert_fn
+    acts, outs, ((dr, dc), (cr, cc)) = emulated_exchange(xs, idxs, ws, placement.owner, sess.P, fn, tdt, acc)
+    rows = 2 * assignment.num_tokens * assignment.topk * token_bytes  # pack + unpack, per direction
+    naive = naive_inter_node_bytes(assignment, placement, topo, token_bytes)
+    d.inter_bytes_total = naive
+    d.groups = c.groups = None
+    drep = PhaseReport("dispatch", mode, 0.0, dr, dc, naive, d.intra_bytes_total, d.intra_gpu_bytes, rows)
+    crep = PhaseReport("combine", mode, 0.0, cr, cc, c.inter_bytes_total, c.intra_bytes_total, c.intra_gpu_bytes,
+                       rows)
+    buffers = None
+    if materialize or mode == "wallclock":
+        buffers = {}
+        for g in range(sess.P):
+            buffers[f"activation/{g}"] = acts[g].contiguous().view(torch.uint8).reshape(-1).cpu().numpy()
+            buffers[f"output/{g}"] = outs[g].contiguous().view(torch.uint8).reshape(-1).cpu().numpy()
+    return ExchangeResult(mode, None, d, c, drep, crep, payloads if buffers is not None else None, buffers)
 
 
 # SPEC.md:396,405 names for the whole-cluster (emulated) execution

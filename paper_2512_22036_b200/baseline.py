@@ -112,3 +112,100 @@ class DisaggregatedShuffle:
     def rearrange_bytes(num_tokens: int, topk: int, token_bytes: int) -> int:
         """Four standalone passes over the routed rows (engine.py:628-630)."""
         return 4 * num_tokens * topk * token_bytes
+
+
+def emulated_exchange(xs, idxs, ws, owner, P: int, expert_fn=None, dtype=torch.float32, acc: str = "f32",
+                      stream_events: bool = True):
+    """Disaggregated shuffle of P emulated ranks on one GPU (the reference's
+    ``run_baseline`` executed with stock torch ops): per source rank an
+    index_select pack into destination-major order, the "all-to-all" as the
+    per-destination concatenation of every source's slice, an index_select
+    unpack into (expert, source, token) order; combine mirrors it and reduces
+    in k order (f64 multiply-then-add with ``acc="f64"``, as engine.py:322-331).
+
+    Returns (activations per rank [rows, H], outputs per rank [T_s, H],
+    (pack+unpack seconds, exchange seconds) per direction).
+    """
+    dev = xs[0].device
+    owner_t = torch.as_tensor(np.asarray(owner), dtype=torch.int64, device=dev)
+    K = idxs[0].shape[1] if idxs else 1
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(9)]
+    ev[0].record()
+    # ---- dispatch: pack per source ----
+    packs, metas, counts = [], [], []
+    for s in range(P):
+        flat_e = idxs[s].reshape(-1).to(torch.int64)
+        dest = owner_t[flat_e]
+        order = torch.argsort(dest, stable=True)
+        tok = torch.div(order, K, rounding_mode="floor")
+        packs.append(xs[s].index_select(0, tok))
+        metas.append((flat_e[order], tok, order))
+        counts.append(torch.bincount(dest, minlength=P).tolist())
+    ev[1].record()
+    # ---- exchange: destination g receives every source's slice, source order ----
+    recv, recv_meta = [], []
+    for g in range(P):
+        parts, e_l, s_l, t_l = [], [], [], []
+        for s in range(P):
+            lo = sum(counts[s][:g])
+            n = counts[s][g]
+            parts.append(packs[s][lo:lo + n])
+            e_l.append(metas[s][0][lo:lo + n])
+            t_l.append(metas[s][1][lo:lo + n])
+            s_l.append(torch.full((n,), s, dtype=torch.int64, device=dev))
+        recv.append(torch.cat(parts) if parts else packs[0][:0])
+        recv_meta.append((torch.cat(e_l), torch.cat(s_l), torch.cat(t_l)))
+    ev[2].record()
+    # ---- unpack into expert-major order ----
+    acts, perms = [], []
+    tmax = max([int(x.shape[0]) for x in xs] + [1]) + 1
+    for g in range(P):
+        e, src, t = recv_meta[g]
+        perm = torch.argsort((e * P + src) * tmax + t)
+        acts.append(recv[g].index_select(0, perm))
+        perms.append(perm)
+    ev[3].record()
+    outs_act = acts
+    if expert_fn is not None:
+        outs_act = []
+        for g in range(P):
+            eids = recv_meta[g][0].index_select(0, perms[g])
+            y = expert_fn(acts[g].to(torch.float32), eids)
+            outs_act.append(y.to(acts[g].dtype))
+    ev[4].record()
+    # ---- combine: back to received order, exchange back, unpack to (t, k) ----
+    back = []
+    for g in range(P):
+        y = torch.empty_like(outs_act[g])
+        y.index_copy_(0, perms[g], outs_act[g])
+        back.append(y)
+    ev[5].record()
+    staged = []
+    for s in range(P):
+        parts = []
+        for g in range(P):
+            lo = sum(counts[q][g] for q in range(s))
+            parts.append(back[g][lo:lo + counts[s][g]])
+        staged.append(torch.cat(parts) if parts else back[0][:0])
+    ev[6].record()
+    outs = []
+    for s in range(P):
+        T = xs[s].shape[0]
+        H = xs[s].shape[1]
+        stg = torch.empty((T * K, H), dtype=staged[s].dtype, device=dev)
+        stg.index_copy_(0, metas[s][2], staged[s])
+        stg = stg.view(T, K, H)
+        w = ws[s]
+        if acc == "f64":
+            out = torch.zeros((T, H), dtype=torch.float64, device=dev)
+            for k in range(K):
+                out = out + w[:, k : k + 1].double() * stg[:, k].double()
+        else:
+            out = torch.zeros((T, H), dtype=torch.float32, device=dev)
+            for k in range(K):
+                out.addcmul_(stg[:, k].float(), w[:, k : k + 1].float())
+        outs.append(out.to(dtype))
+    ev[7].record()
+    torch.cuda.synchronize()
+    t = lambda i, j: ev[i].elapsed_time(ev[j]) * 1e-3  # noqa: E731
+    return acts, outs, ((t(0, 1) + t(2, 3), t(1, 2)), (t(4, 5) + t(6, 7), t(5, 6)))

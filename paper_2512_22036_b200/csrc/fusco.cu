@@ -64,6 +64,7 @@ struct fs_ctx {
   int tma_lag, tma_ctas;
   size_t tma_smem;
   int pdl;              // 1: programmatic dependent launch planner -> dispatch (FUSCO_PDL=0 disables)
+  int nodedup;          // 1: no per-rank dedup on dispatch (FUSCO_NODEDUP=1; planner ablation)
   int comb_minb4;       // warp combine, K <= 2: force 4 CTAs/SM (FUSCO_COMB_MINB4=1)
   int comb_nopipe;      // K <= 2: plain warp combine instead of the pipelined one (FUSCO_COMB_NOPIPE=1)
   int cluster_layout;   // 1: single-cluster DSMEM planner usable (E <= 256, K <= 8)
@@ -99,6 +100,7 @@ FsArgs make_args(const fs_ctx* h, int T, int idx64) {
   a.tb = h->tb;
   a.T = T;
   a.idx64 = idx64;
+  a.nodedup = h->nodedup;
   a.epoch_ptr = h->epoch_d;
   a.max_rows = h->max_rows;
   a.owner = h->owner_d;
@@ -311,6 +313,8 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
   }
   h->sms = sms;
   {
+    const char* nd = getenv("FUSCO_NODEDUP");
+    h->nodedup = nd && std::string(nd) == "1";
     const char* pd = getenv("FUSCO_PDL");
     h->pdl = !(pd && std::string(pd) == "0");
     const char* mb = getenv("FUSCO_COMB_MINB4");

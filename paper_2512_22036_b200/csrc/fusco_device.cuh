@@ -30,6 +30,7 @@ constexpr size_t kOffDone = 1024;      // u64: this rank's dispatch CTAs done pu
 struct FsArgs {
   int rank, world, E, K, tb, T;
   int idx64;      // topk_idx element size 8 (else 4)
+  int nodedup;    // 1: every (token, k) row crosses the link (the reference's "planner" ablation)
   // Iteration counter in device memory (per handle), so a captured CUDA graph
   // replays correctly: fs_layout's LOCAL phase uses *epoch + 1 and stores it;
   // every later phase/kernel of the iteration reads it.  parity = epoch & 1

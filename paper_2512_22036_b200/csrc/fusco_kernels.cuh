@@ -741,7 +741,7 @@ __global__ void __launch_bounds__(kMoveThreads)
       const uint32_t same = __match_any_sync(kFull, g);
       const int first_lane = __ffs(same) - 1;
       const int r_first = __shfl_sync(kFull, r, first_lane);
-      const bool direct = lane < K && r >= 0 && (first_lane == lane || g == s);
+      const bool direct = lane < K && r >= 0 && (a.nodedup || first_lane == lane || g == s);
       const uint32_t dmask = __ballot_sync(kFull, direct);
       if (sl == 0 && lane < K && r >= 0) {
         int32_t* fs = reinterpret_cast<int32_t*>(a.peer[g] + fan_off);
@@ -863,7 +863,7 @@ __global__ void __launch_bounds__(kTmaThreads)
         const uint32_t same = __match_any_sync(kFull, g);
         const int first_lane = __ffs(same) - 1;
         const int r_first = __shfl_sync(kFull, r, first_lane);
-        const bool direct = lane < K && r >= 0 && (first_lane == lane || g == s);
+        const bool direct = lane < K && r >= 0 && (a.nodedup || first_lane == lane || g == s);
         if (lane < K && r >= 0) {
           int32_t* fs = reinterpret_cast<int32_t*>(a.peer[g] + fan_off);
           fs[r] = direct ? r : r_first;

@@ -374,3 +374,30 @@ def test_planner_engines_single_rank(monkeypatch, planner, E, K, T, zipf):
                    first=[plans[0].first_mask.cpu().numpy()], rank_mask=[plans[0].rank_mask.cpu().numpy()],
                    ids=[np.arange(T)])
     _check_layout(res, a, pl, 1)
+
+
+@pytest.mark.parametrize("ablate", [("planner",), ("balancer",), ("dcomm",), ("planner", "dcomm")])
+@pytest.mark.parametrize("name", ["box8_e64k8_scaled", "grid2x2_imbalanced", "box2_e8k2_uniform"])
+def test_run_exchange_ablations_match_reference_golden(name, ablate):
+    """Reference ablations (engine.py:384-420): same bytes, different traffic
+    (no dedup / disaggregated rearrangement passes / static groups)."""
+    pkg = _pkg()
+    g = load_golden(name)
+    topo = pkg.ClusterTopology(g["num_nodes"], g["gpus_per_node"])
+    pl = pkg.ExpertPlacement(g["num_experts"], g["owner"])
+    a = pkg.RoutingAssignment(g["experts"].shape[0], g["topk"], g["experts"], g["weights"], g["source"])
+    fn = pkg.scaled_expert(g["num_experts"]) if g["expert"] == "scaled" else pkg.identity_expert
+    r = pkg.run_exchange(a, topo, pl, g["token_bytes"], payload_seed=g["payload_seed"], expert_fn=fn, ablate=ablate)
+    tb = g["token_bytes"]
+    acts = split_rows(g["activations"], g["act_rows"], tb)
+    outs = split_rows(g["outputs"], g["out_rows"], tb)
+    for rank in range(topo.num_gpus):
+        assert np.array_equal(r.activation(rank).reshape(-1, tb), acts[rank])
+        assert np.array_equal(r.output(rank).reshape(-1, tb), outs[rank])
+    naive = pkg.naive_inter_node_bytes(a, pl, topo, tb)
+    if "planner" in ablate or "dcomm" in ablate:
+        assert r.dispatch_report.inter_node_bytes == naive
+    if "dcomm" in ablate:
+        assert r.dispatch_report.rearrange_bytes + r.combine_report.rearrange_bytes == 4 * a.num_tokens * a.topk * tb
+    else:
+        assert r.dispatch_report.rearrange_bytes == 0
