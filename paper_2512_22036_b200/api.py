@@ -250,6 +250,24 @@ class _Session:
         )
 
 
+def _open_session(assignment, topo, placement, token_bytes, ablate, *, with_act_out, device=None) -> _Session:
+    """A session whose ranks push without dedup when ``planner`` is ablated
+    (every (token, k) row crosses the link; FUSCO_NODEDUP is read at fs_create)."""
+    import os
+
+    if "planner" not in ablate:
+        return _Session(assignment, topo, placement, token_bytes, with_act_out=with_act_out, device=device)
+    prev = os.environ.get("FUSCO_NODEDUP")
+    os.environ["FUSCO_NODEDUP"] = "1"
+    try:
+        return _Session(assignment, topo, placement, token_bytes, with_act_out=with_act_out, device=device)
+    finally:
+        if prev is None:
+            os.environ.pop("FUSCO_NODEDUP", None)
+        else:
+            os.environ["FUSCO_NODEDUP"] = prev
+
+
 def build_plan_pair(
     assignment: RoutingAssignment,
     topo: ClusterTopology,
@@ -334,19 +352,7 @@ def run_exchange(
                                   balancer=balancer, mode=mode, expert_fn=expert_fn, materialize=materialize,
                                   dtype=dtype, acc=acc, device=device)
     identity = expert_fn is identity_expert
-    import os
-
-    prev = os.environ.get("FUSCO_NODEDUP")
-    if "planner" in ablate:  # no dedup: every (token, k) row crosses the link
-        os.environ["FUSCO_NODEDUP"] = "1"
-    try:
-        sess = _Session(assignment, topo, placement, token_bytes, with_act_out=not identity, device=device)
-    finally:
-        if "planner" in ablate:
-            if prev is None:
-                os.environ.pop("FUSCO_NODEDUP", None)
-            else:
-                os.environ["FUSCO_NODEDUP"] = prev
+    sess = _open_session(assignment, topo, placement, token_bytes, ablate, with_act_out=not identity, device=device)
     try:
         cl, P, dev = sess.cluster, sess.P, sess.dev
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]

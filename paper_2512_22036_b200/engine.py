@@ -354,7 +354,10 @@ class EmulatedCluster:
         return (FS_PHASE_ALL,) if self.world == 1 else (FS_PHASE_LOCAL, FS_PHASE_REMOTE)
 
     def layout(self, topk_idx: list[torch.Tensor], with_masks: bool = True) -> list[Plan]:
-        plans = [r.new_plan(t, with_masks) for r, t in zip(self.ranks, topk_idx)]
+        return self.layout_into([r.new_plan(t, with_masks) for r, t in zip(self.ranks, topk_idx)])
+
+    def layout_into(self, plans: list[Plan]) -> list[Plan]:
+        """Re-plan into existing Plan tensors (same routing tensors; e.g. a graph-captured step)."""
         for ph in self._phases():
             for r, p in zip(self.ranks, plans):
                 r.layout(p, ph)

@@ -401,3 +401,27 @@ def test_run_exchange_ablations_match_reference_golden(name, ablate):
         assert r.dispatch_report.rearrange_bytes + r.combine_report.rearrange_bytes == 4 * a.num_tokens * a.topk * tb
     else:
         assert r.dispatch_report.rearrange_bytes == 0
+
+
+@pytest.mark.gpu
+def test_bench_matrix_rows_on_gpu():
+    """§8f next row #2: every variant of a small matrix runs on the GPU and
+    yields schema-valid rows; the planner-off and baseline variants move at
+    least as many link bytes as the fused one (no dedup), the baseline
+    reports its standalone rearrangement bytes (4·T·K·tb)."""
+    from paper_2512_22036_b200 import matrix as M
+
+    topo, pl = _pkg().preset("test")
+    cfg = M.BenchConfig(topo, pl, ("realworld",), (512,), topk=4, token_bytes=256, repeats=1,
+                        variants=tuple(M.VARIANT_ABLATE))
+    doc = M.run_matrix(cfg)
+    M.validate_result(doc)
+    rows = {r["variant"]: r for r in doc["rows"]}
+    assert set(rows) == set(M.VARIANT_ABLATE)
+    for r in rows.values():
+        assert r["total_s"] > 0 and r["latency_us"] > 0
+        assert r["mode"] == ("gpu-eager" if r["variant"] in ("baseline", "dcomm_off") else "gpu-graph")
+    assert rows["fused"]["rearrange_bytes"] == 0
+    assert rows["baseline"]["rearrange_bytes"] == 4 * 512 * 4 * 256
+    assert rows["planner_off"]["inter_node_bytes"] >= rows["fused"]["inter_node_bytes"]
+    assert rows["fused"]["dedup_ratio"] >= 1.0

@@ -156,3 +156,41 @@ def test_no_cpu_fallback_in_product_path():
     for py in pkg.rglob("*.py"):
         src = py.read_text()
         assert "import oracle" not in src and "from oracle" not in src, py
+
+
+def _matrix_cfg():
+    from paper_2512_22036_b200 import matrix as M
+
+    topo, pl = T.preset("test")
+    return M, M.BenchConfig(topo, pl, ("realworld", "imbalanced"), (256, 512), topk=4, token_bytes=64, repeats=1)
+
+
+def test_bench_matrix_cells_fingerprint_and_render():
+    """Matrix structure mirrors the reference (bench.py:48-160): pattern-major
+    cells, per-cell SeedSequence((seed, index)) routing, stable sha256
+    fingerprint that changes with the config, JSON/CSV/MD emitters."""
+    M, cfg = _matrix_cfg()
+    assert M.cells(cfg) == [("realworld", 256), ("realworld", 512), ("imbalanced", 256), ("imbalanced", 512)]
+    a1 = M.cell_assignment(cfg, 1, "realworld", 512)
+    a2 = M.cell_assignment(cfg, 1, "realworld", 512)
+    assert a1.num_tokens == 512 and np.array_equal(a1.experts, a2.experts)
+    assert not np.array_equal(M.cell_assignment(cfg, 0, "realworld", 512).experts, a1.experts)
+    fp = cfg.fingerprint()
+    assert len(fp) == 64 and fp == M.BenchConfig(cfg.topo, cfg.placement, cfg.patterns, cfg.seq_lens, topk=4,
+                                                 token_bytes=64, repeats=1).fingerprint()
+    assert fp != M.BenchConfig(cfg.topo, cfg.placement, cfg.patterns, cfg.seq_lens, topk=4, token_bytes=128,
+                               repeats=1).fingerprint()
+    row = {k: 0 for k in M.ROW_FIELDS}
+    row.update(pattern="realworld", seq_len=16, variant="fused", mode="gpu", balancer="greedy", dedup_ratio=1.5,
+               total_s=1e-5, latency_us=10.0, routed_gbps=1.0)
+    doc = {"schema": M.SCHEMA_ID, "fingerprint": fp, "config": cfg.fingerprint_doc(), "rows": [row]}
+    M.validate_result(doc)
+    assert M.render(doc, "csv").splitlines()[0].split(",") == list(M.ROW_FIELDS)
+    assert "| realworld | 16 | fused |" in M.render(doc, "md")
+    import json
+
+    assert json.loads(M.render(doc, "json"))["rows"][0]["variant"] == "fused"
+    with pytest.raises(ValueError):
+        M.validate_result({**doc, "rows": [{**row, "variant": "nope"}]})
+    with pytest.raises(ValueError):
+        M.validate_result({**doc, "rows": [{k: v for k, v in row.items() if k != "dedup_ratio"}]})
