@@ -64,6 +64,7 @@ struct fs_ctx {
   int tma_lag, tma_ctas;
   size_t tma_smem;
   int pdl;              // 1: programmatic dependent launch planner -> dispatch (FUSCO_PDL=0 disables)
+  int pdl_multi;        // 1: PDL for the cooperative P > 1 movers too (FUSCO_PDL_MULTI=0 disables)
   int nodedup;          // 1: no per-rank dedup on dispatch (FUSCO_NODEDUP=1; planner ablation)
   int comb_minb4;       // warp combine, K <= 2: force 4 CTAs/SM (FUSCO_COMB_MINB4=1)
   int comb_nopipe;      // K <= 2: plain warp combine instead of the pipelined one (FUSCO_COMB_NOPIPE=1)
@@ -136,6 +137,34 @@ bool aligned(const void* p, size_t n) { return (reinterpret_cast<uintptr_t>(p) %
 template <typename Kern>
 int occupancy(Kern kernel, int threads, size_t smem, int* out) {
   FS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, kernel, threads, smem));
+  return FS_OK;
+}
+
+// Launch with optional cooperative (co-residency for cross-CTA waits) and
+// programmatic-dependent-launch attributes (the kernel's prologue overlaps the
+// previous kernel's tail; every kernel griddep_wait()s before reading its
+// predecessor's outputs).
+int launch_ex(const void* fn, int grid, int block, size_t smem, void* stream, void** args, bool coop, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (coop) {
+    attr[n].id = cudaLaunchAttributeCooperative;
+    attr[n].val.cooperative = 1;
+    ++n;
+  }
+  if (pdl) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  FS_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
   return FS_OK;
 }
 
@@ -268,6 +297,10 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
                              (int)h->layout_smem);
     if (e != cudaSuccess) return cleanup(fail(FS_ECUDA, cudaGetErrorString(e)));
   }
+  if (grid_ctas <= 0) {  // experiment knob: cap the mover grids
+    const char* gc = getenv("FUSCO_GRID_CTAS");
+    if (gc) grid_ctas = atoi(gc);
+  }
   int occ_l = 0;
   int rc = occupancy(layout_kernel, kLayoutThreads, h->layout_smem, &occ_l);
   if (rc) return cleanup(rc);
@@ -275,8 +308,8 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
   const int max_chunks = std::max(1, (max_tokens + kLayoutThreads - 1) / kLayoutThreads);
   h->layout_grid_max = std::min(max_chunks, occ_l * sms);
 
-  // Dispatch grid: part of the cross-rank arrival count, so it must be equal
-  // on every rank (same GPU model -> same occupancy -> same grid).
+  // Dispatch grid upper bound (occupancy x SMs); the warp mover sizes each
+  // launch to its work (fs_dispatch), the TMA mover uses the bound.
   int occ_d = 0;
   if ((rc = occupancy(dispatch_kernel<int4>, kMoveThreads, 0, &occ_d))) return cleanup(rc);
   int o = 0;
@@ -317,6 +350,8 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
     h->nodedup = nd && std::string(nd) == "1";
     const char* pd = getenv("FUSCO_PDL");
     h->pdl = !(pd && std::string(pd) == "0");
+    const char* pm = getenv("FUSCO_PDL_MULTI");
+    h->pdl_multi = h->pdl && !(pm && std::string(pm) == "0");
     const char* mb = getenv("FUSCO_COMB_MINB4");
     h->comb_minb4 = mb && std::string(mb) == "1";
     const char* np = getenv("FUSCO_COMB_NOPIPE");
@@ -529,16 +564,19 @@ int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_byte
       return FS_OK;
     }
     void* targs[] = {&a, (void*)&x, (void*)&topk_idx, (void*)&row_of, &phase, &nslots};
-    FS_CUDA(cudaLaunchCooperativeKernel(tfn, dim3(h->move_grid), dim3(kTmaThreads),
-                                        targs, h->tma_smem, (cudaStream_t)stream));
-    return FS_OK;
+    return launch_ex(tfn, h->move_grid, kTmaThreads, h->tma_smem, stream, targs, true, h->pdl_multi);
   }
   void* args[] = {&a, (void*)&x, (void*)&topk_idx, (void*)&row_of, &phase};
   const void* fn = vec16 ? (const void*)dispatch_kernel<int4> : (const void*)dispatch_kernel<int>;
-  // fixed grid per handle: the done counter of a rank reaches epoch * move_grid
-  FS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(h->move_grid), dim3(kMoveThreads), args, 0,
-                                      (cudaStream_t)stream));
-  return FS_OK;
+  // Grid sized to the work: every CTA joins the end-of-push count (one
+  // acq_rel atomic each), so idle CTAs only add latency at decode sizes.
+  // At least one CTA per SM (the receiver fan-out uses the same grid).
+  const int U = vec16 ? 8 : 16, elem = vec16 ? 16 : 4;
+  const long long slices = ((long long)h->tb / elem + 32 * U - 1) / (32 * U);
+  const long long units = (long long)num_tokens * slices;
+  const long long want = (units + kMoveThreads / 32 - 1) / (kMoveThreads / 32);
+  const int grid = (int)std::min<long long>(h->move_grid, std::max<long long>(want, h->sms));
+  return launch_ex(fn, grid, kMoveThreads, 0, stream, args, true, h->pdl_multi);
 }
 
 int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes, const int32_t* row_of, const void* topk_w,
@@ -570,9 +608,7 @@ int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes, const int32_t
             : (f64 ? (const void*)combine_tma_kernel<false, true> : (const void*)combine_tma_kernel<false, false>);
     int ns = h->comb_stages, sb = h->comb_sb;
     void* targs[] = {&a, (void*)&topk_idx, (void*)&row_of, (void*)&topk_w, &w64, &out, &src, &phase, &ns, &sb};
-    FS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(h->comb_grid), dim3(kCombThreads), targs, h->comb_smem,
-                                        (cudaStream_t)stream));
-    return FS_OK;
+    return launch_ex(fn, h->comb_grid, kCombThreads, h->comb_smem, stream, targs, true, h->pdl_multi);
   }
   // rows in flight per unit: min(K, 4) (no registers reserved for loads that never issue)
   if (vec16 && h->K <= 2 && !h->comb_minb4 && !h->comb_nopipe) {
@@ -615,8 +651,7 @@ int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes, const int32_t
   occ = std::max(1, std::min(occ, kMaxCtasPerSm));
   int grid = occ * h->sms;
   if (h->combine_grid_cap > 0) grid = std::min(grid, h->combine_grid_cap);
-  FS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kMoveThreads), args, 0, (cudaStream_t)stream));
-  return FS_OK;
+  return launch_ex(fn, grid, kMoveThreads, 0, stream, args, true, h->pdl_multi);
 }
 
 int fs_check(fs_handle_t h, void* stream) {

@@ -25,7 +25,7 @@ constexpr size_t kSigBytes = 4096;
 constexpr size_t kOffCountFlag = 0;    // u32[FS_MAX_RANKS]: layout counts published
 constexpr size_t kOffReadyFlag = 256;  // u32[FS_MAX_RANKS]: expert outputs ready
 constexpr size_t kOffArrive = 512;     // u32[FS_MAX_RANKS]: source s finished pushing here (epoch)
-constexpr size_t kOffDone = 1024;      // u64: this rank's dispatch CTAs done pushing (epoch * grid)
+constexpr size_t kOffDone = 1024;      // u64: reserved
 
 struct FsArgs {
   int rank, world, E, K, tb, T;
@@ -58,6 +58,7 @@ struct FsArgs {
 constexpr int kWorkDispatch = 0;
 constexpr int kWorkFanout = 1;
 constexpr int kWorkCombine = 2;
+constexpr int kWorkDone = 3;  // dispatch CTAs of this epoch done pushing (target gridDim.x)
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -132,9 +133,12 @@ __device__ __forceinline__ bool wait_u64_geq(const unsigned long long* p, unsign
 __device__ __forceinline__ void signal_pushed(const FsArgs& a, uint32_t epoch) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned long long* done = reinterpret_cast<unsigned long long*>(a.peer[a.rank] + kOffDone);
+    // per-parity counter, zeroed by the planner for the next epoch, so the
+    // grid may differ between launches
+    unsigned long long* done = a.work + (size_t)(epoch & 1u) * 8 + kWorkDone;
     const unsigned long long prev = atom_add_acq_rel_gpu_u64(done, 1ull);
-    if (prev + 1 == (unsigned long long)epoch * gridDim.x) {
+    if (prev + 1 == (unsigned long long)gridDim.x) {
+      if (a.trace != nullptr) a.trace[7] = globaltimer();  // the last CTA's signal
       for (int g = 0; g < a.world; ++g)
         st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[g] + kOffArrive) + a.rank, epoch);
     }

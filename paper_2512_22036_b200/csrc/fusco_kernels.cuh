@@ -79,6 +79,30 @@ __device__ __forceinline__ void block_segmented_base(int E, const int32_t* tot, 
   }
 }
 
+// pre[e] += Σ chunk_cnt[j] over j < n with j % E == e (the counts of the
+// chunks before this one).  When E divides the block size every thread owns
+// one expert column, so its loads are independent and accumulate in a
+// register (one L2 round trip per batch instead of one per element).
+__device__ __forceinline__ void chunk_prefix(const int32_t* cnt, int n, int E, int32_t* pre) {
+  const int tid = threadIdx.x;
+  if (kLayoutThreads % E == 0) {
+    int v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int j = tid;
+    for (; j + 7 * kLayoutThreads < n; j += 8 * kLayoutThreads) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] += ld_cg(cnt + j + q * kLayoutThreads);
+    }
+    for (; j < n; j += kLayoutThreads) v[0] += ld_cg(cnt + j);
+    const int acc = v[0] + v[1] + v[2] + v[3] + v[4] + v[5] + v[6] + v[7];
+    if (acc) atomicAdd(&pre[tid % E], acc);
+  } else {
+    for (int j = tid; j < n; j += kLayoutThreads) {
+      const int v = ld_cg(cnt + j);
+      if (v) atomicAdd(&pre[j % E], v);
+    }
+  }
+}
+
 // ===========================================================================
 // Layout planner
 //
@@ -146,13 +170,26 @@ __global__ void __launch_bounds__(kLayoutThreads)
     const int t0 = c * kLayoutThreads;
     const int nel = min(kLayoutThreads, T - t0) * K;
     const size_t base_el = (size_t)t0 * K;
-    for (int j = tid; j < nel; j += kLayoutThreads) {
-      long long e = load_idx(idx, base_el + j, a.idx64);
-      if (e < 0 || e >= E) {
-        record_error(a.status, FS_ERANGE);
-        e = 0;
+    // 8 independent loads in flight per thread before any is consumed
+    for (int j0 = tid; j0 < nel; j0 += 8 * kLayoutThreads) {
+      long long v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = j0 + q * kLayoutThreads;
+        v[q] = j < nel ? load_idx(idx, base_el + j, a.idx64) : 0;
       }
-      e_s[j] = (int32_t)e;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = j0 + q * kLayoutThreads;
+        if (j < nel) {
+          long long e = v[q];
+          if (e < 0 || e >= E) {
+            record_error(a.status, FS_ERANGE);
+            e = 0;
+          }
+          e_s[j] = (int32_t)e;
+        }
+      }
     }
   };
   if ((phase & FS_PHASE_LOCAL) && (int)blockIdx.x < nchunks) stage_chunk(blockIdx.x);
@@ -172,22 +209,38 @@ __global__ void __launch_bounds__(kLayoutThreads)
       }
       for (int j = tid; j < kLayoutWarps * E; j += kLayoutThreads) bits[j] = 0u;
       __syncthreads();
+      trace_stamp(a, 6);
       const int my_node = node_s[s];
       if (tid < ntok) {
         uint32_t seen_node = 0u, seen_rank = 0u;
-        for (int k = 0; k < K; ++k) {
-          const int e = e_s[tid * K + k];
-          const int g = owner_s[e];
-          const int n = node_s[g];
-          const bool first = !((seen_node >> n) & 1u);
-          seen_node |= 1u << n;
-          seen_rank |= 1u << g;
-          pos_s[tid * K + k] = first ? 1 : 0;  // first_mask staged here until positions overwrite it
-          st_naive += (g != s);
-          st_local += (g == s);
-          st_node += (first && n != my_node);
-          const uint32_t old = atomicOr(&bits[warp * E + e], 1u << lane);
-          if (old & (1u << lane)) record_error(a.status, FS_EINVAL);  // duplicate expert in a row
+        // groups of 8 experts: all smem lookups of a group issue before the
+        // first is consumed (short dependent chains instead of K long ones)
+        for (int k0 = 0; k0 < K; k0 += 8) {
+          int ev[8], gv[8], nv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) ev[q] = (k0 + q < K) ? e_s[tid * K + k0 + q] : 0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) gv[q] = owner_s[ev[q]];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) nv[q] = node_s[gv[q]];
+          uint32_t old[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            old[q] = (k0 + q < K) ? atomicOr(&bits[warp * E + ev[q]], 1u << lane) : 0u;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (k0 + q < K) {
+              const int g = gv[q], n = nv[q];
+              const bool first = !((seen_node >> n) & 1u);
+              seen_node |= 1u << n;
+              seen_rank |= 1u << g;
+              pos_s[tid * K + k0 + q] = first ? 1 : 0;  // first_mask staged here until positions overwrite it
+              st_naive += (g != s);
+              st_local += (g == s);
+              st_node += (first && n != my_node);
+              if (old[q] & (1u << lane)) record_error(a.status, FS_EINVAL);  // duplicate expert in a row
+            }
+          }
         }
         if (rank_mask) rank_mask[t0 + tid] = seen_rank;
         st_dedup += __popc(seen_rank & ~(1u << s));
@@ -208,9 +261,15 @@ __global__ void __launch_bounds__(kLayoutThreads)
       }
       __syncthreads();
       if (tid < ntok) {
-        for (int k = 0; k < K; ++k) {
-          const int e = e_s[tid * K + k];
-          pos_s[tid * K + k] = (int32_t)(wbase[warp * E + e] + __popc(bits[warp * E + e] & lt_mask));
+        for (int k0 = 0; k0 < K; k0 += 8) {
+          int ev[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) ev[q] = (k0 + q < K) ? e_s[tid * K + k0 + q] : 0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (k0 + q < K)
+              pos_s[tid * K + k0 + q] =
+                  (int32_t)(wbase[warp * E + ev[q]] + __popc(bits[warp * E + ev[q]] & lt_mask));
         }
       }
       __syncthreads();
@@ -252,10 +311,6 @@ __global__ void __launch_bounds__(kLayoutThreads)
         }
       }
       for (int e = tid; e < E; e += kLayoutThreads) next_totals[e] = 0;
-      if (stats && tid < 4) {
-        const int slot[4] = {FS_STAT_DEDUP_SEND, FS_STAT_NAIVE_SEND, FS_STAT_LOCAL_ROWS, FS_STAT_NODE_DEDUP};
-        stats[slot[tid]] = *reinterpret_cast<volatile long long*>(stat_acc + tid);
-      }
       if (stats && tid >= 5 && tid < FS_NSTATS) stats[tid] = 0;
       if (tid < 8) {
         next_stats[tid] = 0;
@@ -283,15 +338,13 @@ __global__ void __launch_bounds__(kLayoutThreads)
     // All threads sweep the contiguous [c][E] prefix (coalesced, independent
     // loads) and fold into shared memory.
     const int c_first = blockIdx.x;
+    const bool from_smem = single && (phase & FS_PHASE_LOCAL);
+    const bool one_e = E <= kLayoutThreads;  // one expert column per thread
+    int tv = 0;  // P == 1: this thread's expert total, loaded alongside the chunk prefix
+    if (P == 1 && one_e && tid < E) tv = from_smem ? cnt_s[tid] : ld_cg(totals + tid);
     for (int e = tid; e < E; e += kLayoutThreads) pre[e] = 0;
     __syncthreads();
-    if (c_first < nchunks) {
-      const int nprev = c_first * E;
-      for (int j = tid; j < nprev; j += kLayoutThreads) {
-        const int v = ld_cg(a.chunk_cnt + j);
-        if (v) atomicAdd(&pre[j % E], v);
-      }
-    }
+    if (c_first < nchunks) chunk_prefix(a.chunk_cnt, c_first * E, E, pre);
     if (P > 1) {
       if (tid < P)
         wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffCountFlag) + tid, epoch, a);
@@ -309,14 +362,19 @@ __global__ void __launch_bounds__(kLayoutThreads)
         tot[e] = t;
         before[e] = b;
       }
+    } else if (one_e) {
+      if (tid < E) {
+        tot[tid] = tv;
+        before[tid] = 0;
+      }
     } else {
-      const bool from_smem = single && (phase & FS_PHASE_LOCAL);
       for (int e = tid; e < E; e += kLayoutThreads) {
         tot[e] = from_smem ? cnt_s[e] : ld_cg(totals + e);
         before[e] = 0;
       }
     }
     __syncthreads();
+    trace_stamp(a, 15);
     // base_g(e): exclusive scan of totals over rank g's experts
     int32_t* ex_s = pre + E;  // [E+1]
     block_segmented_base<kLayoutThreads>(E, tot, perm_s, seg_s, owner_s, ex_s, base, warp_tot);
@@ -327,10 +385,7 @@ __global__ void __launch_bounds__(kLayoutThreads)
         __syncthreads();
         for (int e = tid; e < E; e += kLayoutThreads) pre[e] = 0;
         __syncthreads();
-        for (int j = tid; j < c * E; j += kLayoutThreads) {
-          const int v = ld_cg(a.chunk_cnt + j);
-          if (v) atomicAdd(&pre[j % E], v);
-        }
+        chunk_prefix(a.chunk_cnt, c * E, E, pre);
         __syncthreads();
       }
       for (int e = tid; e < E; e += kLayoutThreads) pre[e] += base[e] + before[e];
@@ -352,6 +407,12 @@ __global__ void __launch_bounds__(kLayoutThreads)
         const int e = perm_s[j];
         if (expert_counts) expert_counts[j - jb] = tot[e];
         if (expert_offsets) expert_offsets[j - jb] = base[e];
+      }
+      // the statistics sums (complete since the grid barrier) are read back
+      // last: the round trip stays off the count publication's path
+      if (stats && tid < 4) {
+        const int slot[4] = {FS_STAT_DEDUP_SEND, FS_STAT_NAIVE_SEND, FS_STAT_LOCAL_ROWS, FS_STAT_NODE_DEDUP};
+        stats[slot[tid]] = *reinterpret_cast<volatile long long*>(a.stat_part + parity * 8 + tid);
       }
       if (tid == 0) {
         if (expert_offsets) expert_offsets[je - jb] = rows_total;
@@ -704,6 +765,9 @@ __global__ void __launch_bounds__(kMoveThreads)
   const int lane = threadIdx.x & 31;
   const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  __shared__ int32_t owner_sm[kMaxExperts];
+  if (phase & FS_PHASE_LOCAL) load_owner_table(a, owner_sm);  // static table: before the PDL wait
+  griddep_wait();  // row_of / the epoch come from the planner
   const uint32_t epoch = load_epoch(a);
   const int parity = (int)(epoch & 1u);
   const size_t act_off = a.off_act + (size_t)parity * a.act_stride;
@@ -711,8 +775,6 @@ __global__ void __launch_bounds__(kMoveThreads)
   trace_stamp(a, FS_TRACE_DISPATCH_BEGIN);
 
   if (phase & FS_PHASE_LOCAL) {
-    __shared__ int32_t owner_sm[kMaxExperts];
-    load_owner_table(a, owner_sm);
     const long long units = (long long)T * S;
     unsigned long long* ctr = work_ctr(a, epoch, kWorkDispatch);
     long long u = claim_warp(ctr);
@@ -769,6 +831,7 @@ __global__ void __launch_bounds__(kMoveThreads)
     }
     if (P > 1) signal_pushed(a, epoch);
   }
+  griddep_launch_dependents();  // the combine may start its prologue
 
   trace_stamp(a, FS_TRACE_DISPATCH_PUSHED);
   if ((phase & FS_PHASE_REMOTE) && P > 1) {
@@ -957,6 +1020,7 @@ __global__ void __launch_bounds__(kMoveThreads, MINB)
   const int lane = threadIdx.x & 31;
   const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  griddep_wait();  // rows / the epoch from the previous kernel (PDL launch)
   const uint32_t epoch = load_epoch(a);
   const size_t src_off =
       src_sel == FS_SRC_ACT_OUT ? a.off_actout : a.off_act + (size_t)(epoch & 1u) * a.act_stride;
@@ -1261,6 +1325,18 @@ __global__ void __launch_bounds__(kCombThreads)
   const int S = (tb + sb - 1) / sb;
   const int stage_bytes = K * sb;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool remote = (phase & FS_PHASE_REMOTE) != 0;
+  if (remote) {  // prologue independent of the previous kernel (PDL launch)
+    for (int e = threadIdx.x; e < a.E; e += blockDim.x) owner_cmb[e] = a.owner[e];
+    if (threadIdx.x == 0) {
+      for (int q = 0; q < nstages; ++q) {
+        mbar_init(&full[q], 1);
+        mbar_init(&empty[q], kCombConsumers);
+      }
+      mbar_fence_init();
+    }
+  }
+  griddep_wait();  // dispatched rows / the epoch
   const uint32_t epoch = load_epoch(a);
   const size_t src_off =
       src_sel == FS_SRC_ACT_OUT ? a.off_actout : a.off_act + (size_t)(epoch & 1u) * a.act_stride;
@@ -1270,15 +1346,7 @@ __global__ void __launch_bounds__(kCombThreads)
     if (blockIdx.x == 0 && threadIdx.x < P)
       st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[threadIdx.x] + kOffReadyFlag) + s, epoch);
   }
-  if (!(phase & FS_PHASE_REMOTE)) return;
-  for (int e = threadIdx.x; e < a.E; e += blockDim.x) owner_cmb[e] = a.owner[e];
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < nstages; ++q) {
-      mbar_init(&full[q], 1);
-      mbar_init(&empty[q], kCombConsumers);
-    }
-    mbar_fence_init();
-  }
+  if (!remote) return;
   if (P > 1 && threadIdx.x < P)
     wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffReadyFlag) + threadIdx.x, epoch, a);
   __syncthreads();

@@ -37,7 +37,7 @@ tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
 x = torch.randn(T_l, hidden, device=dev).to(tdt)
 idx = torch.as_tensor(a.experts[sel], device=dev)
 w = torch.as_tensor(a.weights[sel], dtype=torch.float32, device=dev)
-names = {0: "layout.begin", 1: "layout.hist", 2: "layout.gridsync", 3: "layout.publish", 4: "layout.wait",
+names = {0: "layout.begin", 6: "layout.staged", 7: "dispatch.signal", 1: "layout.hist", 15: "layout.totals", 2: "layout.gridsync", 3: "layout.publish", 4: "layout.wait",
          5: "layout.end", 8: "dispatch.begin", 9: "dispatch.pushed", 10: "dispatch.arrived", 11: "dispatch.end",
          12: "combine.begin", 13: "combine.ready", 14: "combine.end"}
 lib = _lib.load()
@@ -46,6 +46,34 @@ for it in range(30):
     buf.dispatch(x, plan)
     out = buf.combine(plan, w, src="act")
 torch.cuda.synchronize()
+if os.environ.get("TRACE_GRAPH") == "1":  # replay steps as one CUDA graph: no host gaps between kernels
+    from paper_2512_22036_b200._lib import FS_PHASE_ALL, FS_SRC_ACT
+
+    h = buf.r.handle
+    P_ = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    side = torch.cuda.Stream()
+    st = ctypes.c_void_p(side.cuda_stream)
+    lay = (h, P_(idx), idx.element_size(), idx.shape[0], P_(plan.row_of), P_(plan.expert_counts),
+           P_(plan.expert_offsets), None, None, P_(plan.stats), FS_PHASE_ALL, st)
+    disp = (h, P_(x), P_(idx), idx.element_size(), P_(plan.row_of), idx.shape[0], FS_PHASE_ALL, st)
+    comb = (h, P_(idx), idx.element_size(), P_(plan.row_of), P_(w), 4, idx.shape[0], P_(out), buf.dtype_code,
+            FS_SRC_ACT, 0, FS_PHASE_ALL, st)
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(g, stream=side):
+            for _ in range(4):
+                lib.fs_layout(*lay)
+                lib.fs_dispatch(*disp)
+                lib.fs_combine(*comb)
+    torch.cuda.current_stream().wait_stream(side)
+    for _ in range(5):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        g.replay()
+    torch.cuda.synchronize()
+    buf.check()
 tr = (ctypes.c_uint64 * 16)()
 _lib.call("fs_trace", buf.r.handle, tr, _lib.stream_ptr())
 t = np.array(list(tr), dtype=np.int64)
@@ -56,7 +84,7 @@ if world > 1:  # common time origin: min layout.begin over ranks (globaltimer is
     dist.all_reduce(tt, op=dist.ReduceOp.MIN)
     t0 = int(tt.item())
 prev = t0
-for k in sorted(names):
+for k in sorted(names, key=lambda k: t[k] if t[k] else 1 << 62):
     if t[k]:
         lines.append(f"  {names[k]:18s} {(t[k] - t0) / 1e3:9.2f} us  (+{(t[k] - prev) / 1e3:7.2f})")
         prev = t[k]
