@@ -48,6 +48,8 @@ CONFIGS = {
                     "DeepSeek-V3 decode batch: hidden 7168 bf16, 256 experts top-8, 128 tokens/rank, EP=N"),
     "dsv3_zipf": (7168, "bf16", 256, 8, 4096, 1.2,
                   "DeepSeek-V3 shape under Zipf s=1.2 routing, 4096 tokens/rank, EP=N"),
+    # diagnostic: top-1, so dispatch push bytes == combine pull bytes (no dedup, no fan-out)
+    "k1": (7168, "bf16", 8, 1, 8192, 0.0, "diagnostic: hidden 7168 bf16, 8 experts top-1, 8192 tokens/rank"),
 }
 DEFAULT_CONFIG = "mixtral"  # BASELINE.json configs[1]
 

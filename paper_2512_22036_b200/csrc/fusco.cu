@@ -86,6 +86,7 @@ struct fs_ctx {
   int* num_rows_d;
   uint32_t* epoch_d;  // device iteration counter (graph-replay safe)
   unsigned long long* work_d;  // [2][8] dynamic work counters
+  int2* fan_list_d;            // [max_rows] fan-out list (P > 1)
   unsigned long long* trace_d;  // FS_NTRACE stamps when FUSCO_TRACE=1, else null
 };
 
@@ -124,6 +125,7 @@ FsArgs make_args(const fs_ctx* h, int T, int idx64) {
   a.timeout_ns = h->timeout_ns;
   a.trace = h->trace_d;
   a.work = h->work_d;
+  a.fan_list = h->fan_list_d;
   return a;
 }
 
@@ -412,7 +414,8 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
       (e = dalloc((void**)&h->status_d, 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->num_rows_d, 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->epoch_d, 4)) != cudaSuccess ||
-      (e = dalloc((void**)&h->work_d, 2 * 8 * 8)) != cudaSuccess)
+      (e = dalloc((void**)&h->work_d, 2 * 8 * 8)) != cudaSuccess ||
+      (world > 1 && (e = dalloc((void**)&h->fan_list_d, (size_t)max_rows * sizeof(int2))) != cudaSuccess))
     return cleanup(fail(FS_ECUDA, std::string("fs_create alloc: ") + cudaGetErrorString(e)));
   if ((e = cudaMemcpy(h->owner_d, owner.data(), num_experts * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(h->node_of_d, nodes.data(), world * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
@@ -452,6 +455,7 @@ int fs_destroy(fs_handle_t h) {
   cudaFree(h->num_rows_d);
   cudaFree(h->epoch_d);
   cudaFree(h->work_d);
+  if (h->fan_list_d) cudaFree(h->fan_list_d);
   if (h->trace_d) cudaFree(h->trace_d);
   delete h;
   return FS_OK;

@@ -52,6 +52,7 @@ struct FsArgs {
   unsigned long long timeout_ns;
   unsigned long long* trace;  // optional globaltimer stamps (FUSCO_TRACE=1), see FS_TRACE_*
   unsigned long long* work;   // [2][8] per-parity dynamic work counters (zeroed one epoch ahead)
+  int2* fan_list;             // [max_rows] receiver fan-out list (row, primary row), P > 1
 };
 
 // dynamic work counters (slot within work[parity][*])

@@ -721,10 +721,14 @@ __device__ __forceinline__ void warp_copy_row_cg(V* __restrict__ dst, const V* _
 
 // Receiver-side fan-out: rows whose fan_src points at another row (a
 // duplicate destination of a token that crossed NVLink once) are copied from
-// that primary row, in (row, slice) units spread over every warp of the grid
-// so a few duplicate-heavy row ranges cannot serialise on a few warps.
+// that primary row.  Two steps over the whole (cooperative) grid: every warp
+// scans 32 rows per load (most rows are primaries) and appends the
+// duplicates to a list with one atomic per warp; after a grid barrier the
+// (row, slice) copy units of the list are strided over every warp.  Balanced
+// whatever the duplicates' distribution over the rows (sources, experts).
 template <typename V>
-__device__ __forceinline__ void fan_out_rows(const FsArgs& a, size_t act_off, size_t fan_off, int nv) {
+__device__ __forceinline__ void fan_out_rows(const FsArgs& a, size_t act_off, size_t fan_off, int nv,
+                                             uint32_t epoch) {
   constexpr int U = MoveCfg<V>::U;
   constexpr int SW = 32 * U;
   const int lane = threadIdx.x & 31;
@@ -734,15 +738,27 @@ __device__ __forceinline__ void fan_out_rows(const FsArgs& a, size_t act_off, si
   const int S = (nv + SW - 1) / SW;
   const int32_t* fs = reinterpret_cast<const int32_t*>(a.peer[a.rank] + fan_off);
   V* act = reinterpret_cast<V*>(a.peer[a.rank] + act_off);
-  const long long units = (long long)rows * S;
-  // static striding: most units are no-ops (f == r), a claim per unit would cost more than it balances
+  unsigned long long* cnt = work_ctr(a, epoch, kWorkFanout);
+  const uint32_t lt = (1u << lane) - 1u;
+  for (long long b = gw * 32; b < rows; b += nw * 32) {
+    const int r = (int)b + lane;
+    const int f = r < rows ? ld_cg(fs + r) : r;
+    const bool dup = r < rows && f != r && f >= 0 && f < rows;
+    const uint32_t m = __ballot_sync(kFull, dup);
+    if (m) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(cnt, (unsigned long long)__popc(m));
+      base = __shfl_sync(kFull, base, 0);
+      if (dup) a.fan_list[base + __popc(m & lt)] = make_int2(r, f);
+    }
+  }
+  cg::this_grid().sync();
+  const long long units = (long long)*reinterpret_cast<volatile unsigned long long*>(cnt) * S;
   for (long long u = gw; u < units; u += nw) {
-    const int r = (int)(u / S), sl = (int)(u - (long long)r * S);
-    const int f = ld_cg(fs + r);
-    if (f == r || f < 0 || f >= rows) continue;  // warp-uniform
-    const int w0 = sl * SW, rem = nv - w0;
-    const V* src = act + (size_t)f * nv + w0;
-    V* dst = act + (size_t)r * nv + w0;
+    const int2 rf = __ldcg(a.fan_list + u / S);
+    const int w0 = (int)(u % S) * SW, rem = nv - w0;
+    const V* src = act + (size_t)rf.y * nv + w0;
+    V* dst = act + (size_t)rf.x * nv + w0;
     V v[U];
 #pragma unroll
     for (int j = 0; j < U; ++j)
@@ -839,7 +855,7 @@ __global__ void __launch_bounds__(kMoveThreads)
       wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffArrive) + threadIdx.x, epoch, a);
     __syncthreads();
     trace_stamp(a, FS_TRACE_DISPATCH_ARRIVED);
-    fan_out_rows<V>(a, act_off, fan_off, nv);
+    fan_out_rows<V>(a, act_off, fan_off, nv, epoch);
   }
   trace_stamp(a, FS_TRACE_DISPATCH_END);
 }
@@ -955,7 +971,7 @@ __global__ void __launch_bounds__(kTmaThreads)
       wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffArrive) + threadIdx.x, epoch, a);
     __syncthreads();
     trace_stamp(a, FS_TRACE_DISPATCH_ARRIVED);
-    fan_out_rows<int4>(a, act_off, fan_off, tb / 16);
+    fan_out_rows<int4>(a, act_off, fan_off, tb / 16, epoch);
   }
   trace_stamp(a, FS_TRACE_DISPATCH_END);
 }
