@@ -47,6 +47,20 @@ __device__ __forceinline__ void block_segmented_base(int E, const int32_t* tot, 
                                                      int32_t* ex_s, int32_t* base, int* warp_tot) {
   constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (E <= 32) {  // one warp scans, one barrier
+    if (warp == 0) {
+      const int v = lane < E ? tot[perm_s[lane]] : 0;
+      const int incl = warp_incl_scan(v, lane);
+      if (lane < E) ex_s[lane] = incl - v;
+      if (lane == E - 1) ex_s[E] = incl;
+    }
+    __syncthreads();
+    if (tid < E) {
+      const int e = perm_s[tid];
+      base[e] = ex_s[tid] - ex_s[seg_s[owner_s[e]]];
+    }
+    return;
+  }
   const int per = (E + NT - 1) / NT;  // consecutive elements per thread
   const int j0 = tid * per;
   int loc = 0;
@@ -276,19 +290,22 @@ __global__ void __launch_bounds__(kLayoutThreads)
       if (!keep_pos)
         for (int j = tid; j < nel; j += kLayoutThreads) row_of[base_el + j] = pos_s[j];
     }
-    // statistics: block reduce, then one commutative atomic per counter
-    long long v[4] = {st_dedup, st_naive, st_local, st_node};
+    // statistics: block reduce, then one commutative atomic per counter (a
+    // single rank's are constants: every row is local, nothing is sent)
+    if (P > 1) {
+      long long v[4] = {st_dedup, st_naive, st_local, st_node};
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < 4; ++j) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_xor_sync(kFull, v[j], o);
-      if (lane == 0) red[warp][j] = v[j];
-    }
-    __syncthreads();
-    if (tid < 4) {
-      long long acc = 0;
-      for (int w = 0; w < kLayoutWarps; ++w) acc += red[w][tid];
-      if (acc) atomicAdd(reinterpret_cast<unsigned long long*>(stat_acc + tid), (unsigned long long)acc);
+        for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_xor_sync(kFull, v[j], o);
+        if (lane == 0) red[warp][j] = v[j];
+      }
+      __syncthreads();
+      if (tid < 4) {
+        long long acc = 0;
+        for (int w = 0; w < kLayoutWarps; ++w) acc += red[w][tid];
+        if (acc) atomicAdd(reinterpret_cast<unsigned long long*>(stat_acc + tid), (unsigned long long)acc);
+      }
     }
     trace_stamp(a, FS_TRACE_LAYOUT_HIST);
     if (single) __syncthreads();
@@ -412,7 +429,8 @@ __global__ void __launch_bounds__(kLayoutThreads)
       // last: the round trip stays off the count publication's path
       if (stats && tid < 4) {
         const int slot[4] = {FS_STAT_DEDUP_SEND, FS_STAT_NAIVE_SEND, FS_STAT_LOCAL_ROWS, FS_STAT_NODE_DEDUP};
-        stats[slot[tid]] = *reinterpret_cast<volatile long long*>(a.stat_part + parity * 8 + tid);
+        stats[slot[tid]] = P > 1 ? *reinterpret_cast<volatile long long*>(a.stat_part + parity * 8 + tid)
+                                 : (tid == 2 ? (long long)T * K : 0ll);
       }
       if (tid == 0) {
         if (expert_offsets) expert_offsets[je - jb] = rows_total;
