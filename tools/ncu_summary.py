@@ -17,7 +17,8 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 PROF = ROOT / "profiles"
 FS_NAME = {"layout_kernel": "fs_layout", "dispatch_kernel": "fs_dispatch", "dispatch_tma_kernel": "fs_dispatch",
-           "combine_kernel": "fs_combine", "combine_tma_kernel": "fs_combine"}
+           "combine_kernel": "fs_combine", "combine_tma_kernel": "fs_combine",
+           "combine_k2_kernel": "fs_combine"}
 METRICS = [
     ("gpu__time_duration.sum", "duration", "us", 1e-3),
     ("dram__bytes_read.sum", "DRAM read", "MB", 1e-6),
