@@ -55,8 +55,10 @@ def main():
     stream = _lib.stream_ptr()
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     res = {}
-    for mode, name in ((0, "warp"), (1, "tma")):
-        ctas = sms * (4 if mode == 0 else 8)
+    sweep = os.environ.get("PROBE_SWEEP")  # e.g. "1,2,4,8": warp-mode CTAs per SM to try
+    modes = [(0, f"warp{m}", sms * int(m)) for m in sweep.split(",")] if sweep else \
+        [(0, "warp", sms * 4), (1, "tma", sms * 8)]
+    for mode, name, ctas in modes:
         cases = {
             "hbm": ([recv(rank, 0)], [send(rank, 0)], 2),
             "push": ([recv(g, rank) for g in range(world) if g != rank],
@@ -86,6 +88,42 @@ def main():
                 dist.all_reduce(ms, op=dist.ReduceOp.MAX)
             gbs = factor * len(dsts) * per / (ms.item() * 1e-3) / 1e9
             res[f"{name}_{cname}_gbs"] = round(gbs, 1)
+    if world > 1 and os.environ.get("PROBE_MIXED") == "1":
+        # half of every pair's bytes pushed by the source, half pulled by the
+        # destination, concurrently on two streams: same link direction
+        half = per // 2
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        pd = [recv(g, rank) for g in range(world) if g != rank]
+        ps = [send(rank, g) for g in range(world) if g != rank]
+        ld = [recv(rank, g) + half for g in range(world) if g != rank]
+        ls = [send(g, rank) + half for g in range(world) if g != rank]
+        PD, PS = (c_void_p * len(pd))(*pd), (c_void_p * len(ps))(*ps)
+        LD, LS = (c_void_p * len(ld))(*ld), (c_void_p * len(ls))(*ls)
+        for mode, name in ((0, "warp"), (1, "tma")):
+            ctas = sms * (2 if mode == 0 else 4)
+
+            def go():
+                _lib.call("fs_probe_a2a", local, PD, PS, len(pd), half, mode, ctas, c_void_p(s1.cuda_stream))
+                _lib.call("fs_probe_a2a", local, LD, LS, len(ld), half, mode, ctas, c_void_p(s2.cuda_stream))
+            for _ in range(3):
+                go()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 10
+            cur = torch.cuda.current_stream()
+            e0.record(cur)
+            s1.wait_stream(cur)
+            s2.wait_stream(cur)
+            for _ in range(reps):
+                go()
+            cur.wait_stream(s1)
+            cur.wait_stream(s2)
+            e1.record(cur)
+            torch.cuda.synchronize()
+            ms = torch.tensor([e0.elapsed_time(e1) / reps], device="cuda")
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            res[f"{name}_mixed_gbs"] = round(len(pd) * per / (ms.item() * 1e-3) / 1e9, 1)
     if rank == 0:
         print(json.dumps({"world": world, "mib_per_pair": mib, **res}), flush=True)
     if world > 1:
