@@ -57,6 +57,11 @@ _LAZY = {
     "EmulatedCluster": "engine",
     "Rank": "engine",
     "Plan": "engine",
+    "plan_to_json": "wire",
+    "descriptor_to_bytes": "wire",
+    "descriptor_from_bytes": "wire",
+    "run_matrix": "matrix",
+    "BenchConfig": "matrix",
 }
 
 

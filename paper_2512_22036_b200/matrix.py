@@ -242,10 +242,24 @@ def main(argv=None) -> int:
     ap.add_argument("--out", default="-")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--repeats", type=int, default=3)
+    ap.add_argument("--dump-plan", default=None, metavar="PATH",
+                    help="also write the first cell's device plans as plan_to_json documents (bench.py:399-421)")
     args = ap.parse_args(argv)
     topo, pl = preset(args.preset)
     cfg = BenchConfig(topo, pl, tuple(args.patterns), tuple(args.seq_lens), args.topk, args.token_bytes,
                       balancer=args.balancer, variants=tuple(args.variants), seed=args.seed, repeats=args.repeats)
+    if args.dump_plan:
+        from .api import run_exchange
+        from .wire import plan_to_json
+
+        first = cells(cfg)[0]
+        res = run_exchange(cell_assignment(cfg, 0, *first), cfg.topo, cfg.placement, cfg.token_bytes,
+                           balancer=cfg.balancer, materialize=False, dtype=cfg.dtype, acc="f32")
+        m = cfg.topo.gpus_per_node
+        with open(args.dump_plan, "w") as fh:
+            json.dump({"dispatch": plan_to_json(res.dispatch_plan, m), "combine": plan_to_json(res.combine_plan, m)},
+                      fh, indent=2, sort_keys=True)
+            fh.write("\n")
     doc = run_matrix(cfg)
     validate_result(doc)
     text = render(doc, args.format)

@@ -425,3 +425,30 @@ def test_bench_matrix_rows_on_gpu():
     assert rows["baseline"]["rearrange_bytes"] == 4 * 512 * 4 * 256
     assert rows["planner_off"]["inter_node_bytes"] >= rows["fused"]["inter_node_bytes"]
     assert rows["fused"]["dedup_ratio"] >= 1.0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", golden_names())
+def test_device_plan_json_matches_oracle_plan(name):
+    """§8f #4: the --dump-plan document of the device-built plans (layouts,
+    per-(source, destination) transfers and local edges as descriptor wire
+    blobs) is identical to the one derived from the reference layouts."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from test_host_api import _oracle_plans
+
+    from paper_2512_22036_b200 import wire as W
+
+    pkg = _pkg()
+    g = load_golden(name)
+    topo = pkg.ClusterTopology(g["num_nodes"], g["gpus_per_node"])
+    pl = pkg.ExpertPlacement(int(g["num_experts"]), g["owner"])
+    a = pkg.RoutingAssignment(g["experts"].shape[0], g["topk"], g["experts"], g["weights"], g["source"])
+    d, c, _ = pkg.build_plan_pair(a, topo, pl, g["token_bytes"])
+    od, oc, _, _ = _oracle_plans(g)
+    m = g["gpus_per_node"]
+    for got, want in ((W.plan_to_json(d, m), W.plan_to_json(od, m)), (W.plan_to_json(c, m), W.plan_to_json(oc, m))):
+        for key in ("layouts", "node_transfers", "local_edges", "direction", "topk", "token_bytes"):
+            assert got[key] == want[key], key

@@ -194,3 +194,140 @@ def test_bench_matrix_cells_fingerprint_and_render():
         M.validate_result({**doc, "rows": [{**row, "variant": "nope"}]})
     with pytest.raises(ValueError):
         M.validate_result({**doc, "rows": [{k: v for k, v in row.items() if k != "dedup_ratio"}]})
+
+
+# ---- wire / golden formats (§8f #4) -----------------------------------------
+
+
+def test_descriptor_wire_format():
+    """descriptor.py:224-241: LE u64 count, then (offset, length) u64 pairs."""
+    import struct
+
+    from paper_2512_22036_b200 import wire as W
+
+    blob = W.descriptor_to_bytes([8, 0], [4, 4])
+    assert blob == struct.pack("<QQQQQ", 2, 8, 4, 0, 4)
+    off, ln = W.descriptor_from_bytes(blob)
+    assert off.tolist() == [8, 0] and ln.tolist() == [4, 4]
+    assert W.descriptor_from_bytes(W.descriptor_to_bytes([], []))[0].size == 0
+    with pytest.raises(ValueError):
+        W.descriptor_from_bytes(b"\x01\x00")
+    with pytest.raises(ValueError):
+        W.descriptor_from_bytes(blob[:-1])
+    with pytest.raises(ValueError):
+        W.descriptor_to_bytes([1, 2], [3])
+    ref = Path("/root/reference/pkg/src")
+    if ref.is_dir():  # the reference's own encoder, when present in this container
+        import sys
+
+        sys.path.insert(0, str(ref))
+        try:
+            from shuffleforge.descriptor import DescriptorList
+        finally:
+            sys.path.remove(str(ref))
+        d = DescriptorList("x", np.array([8, 0, 96]), np.array([4, 4, 32]))
+        assert d.to_bytes() == W.descriptor_to_bytes([8, 0, 96], [4, 4, 32])
+
+
+def _oracle_plans(g):
+    """GpuPlan pair built from the oracle's layouts (what the device plan must equal)."""
+    from oracle import shuffle_oracle as O
+    from paper_2512_22036_b200.api import ActivationLayout, GpuPlan
+
+    P = g["num_nodes"] * g["gpus_per_node"]
+    lays, row_of = O.activation_layouts(g["experts"], g["source"], g["owner"], P)
+    layouts = {r: ActivationLayout(l.expert_ids, l.token_ids, l.src, l.k_col) for r, l in lays.items()}
+    local = {s: np.flatnonzero(g["source"] == s) for s in range(P)}
+    tb, K, T = g["token_bytes"], g["topk"], g["experts"].shape[0]
+
+    def mk(direction):
+        return GpuPlan(direction=direction, token_bytes=tb, num_tokens=T, topk=K, groups=None, layouts=layouts,
+                       local_tokens=local, row_of=row_of, first_mask=g["first_mask"], reduce_weights=None,
+                       inter_bytes_total=0, intra_bytes_total=0, intra_gpu_bytes=0, buffer_bytes={},
+                       loads=g["loads"])
+    return mk("dispatch"), mk("combine"), lays, row_of
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_plan_json_executes_to_reference_bytes(name):
+    """The dumped plan (reference plan_to_json schema) is executable: applying
+    its descriptor tables moves exactly the reference's bytes — dispatch
+    activations equal the golden ones, every row written once, each token sent
+    once per destination rank; combine staging reduces to the golden outputs."""
+    import base64
+
+    from oracle import shuffle_oracle as O
+    from paper_2512_22036_b200 import wire as W
+
+    g = load_golden(name)
+    tb, K, T = g["token_bytes"], g["topk"], g["experts"].shape[0]
+    P = g["num_nodes"] * g["gpus_per_node"]
+    dplan, cplan, lays, row_of = _oracle_plans(g)
+    dj = W.plan_to_json(dplan, g["gpus_per_node"])
+    # layouts: exactly the reference's (golden rows concatenated over ranks)
+    for key, gk in (("expert_ids", "lay_expert_ids"), ("token_ids", "lay_token_ids"), ("k_col", "lay_k_col")):
+        got = np.concatenate([np.asarray(dj["layouts"][str(r)][key], dtype=np.int64) for r in range(P)])
+        assert np.array_equal(got, g[gk])
+    tables = lambda d: W.descriptor_from_bytes(base64.b64decode(d["table"]))  # noqa: E731
+    payload = O.encode(np.random.default_rng(0).standard_normal((T, tb // 4)).astype(np.float32), "f32")
+    bufs = {f"token/{s}": payload[np.flatnonzero(g["source"] == s)].reshape(-1).copy() for s in range(P)}
+    for r in range(P):
+        bufs[f"activation/{r}"] = np.zeros(lays[r].num_rows * tb, dtype=np.uint8)
+    written = {r: np.zeros(lays[r].num_rows, dtype=np.int64) for r in range(P)}
+    sent = np.zeros((T, P), dtype=np.int64)
+
+    def apply(item):
+        so, sl = tables(item["send"])
+        ro, rl = tables(item["recv"])
+        assert (sl == tb).all() and (rl == tb).all() and so.size == ro.size
+        src, dst = bufs[item["send"]["buffer"]], bufs[item["recv"]["buffer"]]
+        for a, b in zip(so, ro):
+            dst[b : b + tb] = src[a : a + tb]
+        if item["recv"]["buffer"].startswith("activation/"):
+            written[int(item["recv"]["buffer"].split("/")[1])][ro // tb] += 1
+        return so
+
+    for tr in dj["node_transfers"]:
+        so = apply(tr)
+        toks = np.flatnonzero(g["source"] == tr["src_flat"])[so // tb]
+        sent[toks, tr["dst_flat"]] += 1
+        assert tr["bytes"] == so.size * tb
+    for nd in sorted(dj["local_edges"]):
+        for e in dj["local_edges"][nd]:
+            if e["send"]["buffer"].startswith("token/"):
+                apply(e)
+    for nd in sorted(dj["local_edges"]):  # receiver fan-out after the primaries landed
+        for e in dj["local_edges"][nd]:
+            if e["send"]["buffer"].startswith("activation/"):
+                apply(e)
+    acts = O.dispatch(payload, lays)
+    for r in range(P):
+        assert np.array_equal(bufs[f"activation/{r}"].reshape(-1, tb), acts[r])
+        assert (written[r] == 1).all()
+    own = g["owner"][g["experts"]]
+    want_sent = np.zeros((T, P), dtype=np.int64)
+    for t in range(T):
+        for d in set(own[t].tolist()) - {int(g["source"][t])}:
+            want_sent[t, d] = 1
+    assert np.array_equal(sent, want_sent)  # once per (token, remote rank)
+
+    cj = W.plan_to_json(cplan, g["gpus_per_node"])
+    staging = {s: np.zeros(((g["source"] == s).sum() * K) * tb, dtype=np.uint8) for s in range(P)}
+    act_out = {f"act_out/{r}": acts[r].reshape(-1) for r in range(P)}
+    items = cj["node_transfers"] + [e for nd in cj["local_edges"] for e in cj["local_edges"][nd]]
+    for it in items:
+        so, _ = tables(it["send"])
+        ro, _ = tables(it["recv"])
+        src = act_out[it["send"]["buffer"]]
+        dst = staging[int(it["recv"]["buffer"].split("/")[1])]
+        for a, b in zip(so, ro):
+            dst[b : b + tb] = src[a : a + tb]
+    assert sum(it["bytes"] for it in items) == T * K * tb
+    for s in range(P):
+        ids = np.flatnonzero(g["source"] == s)
+        stg = O.decode(staging[s].reshape(-1, tb), "f32").reshape(ids.size, K, -1).astype(np.float64)
+        out = np.zeros((ids.size, tb // 4), dtype=np.float64)
+        for k in range(K):
+            out = out + g["weights"][ids, k : k + 1] * stg[:, k]
+        want = O.combine(acts, row_of, g["experts"], g["weights"], g["owner"], ids, "f32")
+        assert np.array_equal(O.encode(out.astype(np.float32), "f32"), want)
