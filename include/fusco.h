@@ -141,6 +141,11 @@ int fs_buffer_ptr(fs_handle_t h, int which, void** ptr_out);
 long long fs_max_rows(fs_handle_t h);
 /* Current epoch (incremented by every fs_layout with the LOCAL phase). */
 unsigned int fs_epoch(fs_handle_t h);
+/* Per-rank dispatch dedup on (0, default) or off (1: every (token, k) row
+ * crosses the link) — the reference's "planner" ablation (engine.py:384-420,
+ * build_direct_plans planner.py:563-659).  Takes effect from the next
+ * fs_dispatch; set it identically on every rank. */
+int fs_set_nodedup(fs_handle_t h, int on);
 
 /* ---- the hot path --------------------------------------------------------- */
 

@@ -47,6 +47,7 @@ SIGNATURES = {
     "fs_buffer_ptr": (c_int, [c_void_p, c_int, POINTER(c_void_p)]),
     "fs_max_rows": (c_longlong, [c_void_p]),
     "fs_epoch": (c_uint, [c_void_p]),
+    "fs_set_nodedup": (c_int, [c_void_p, c_int]),
     "fs_layout": (
         c_int,
         [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

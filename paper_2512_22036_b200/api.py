@@ -181,7 +181,7 @@ def _validate(assignment, topo, placement, token_bytes, mode="analytic", ablate=
 class _Session:
     """Routing of a global assignment split into per-rank device tensors."""
 
-    def __init__(self, assignment, topo, placement, token_bytes, *, with_act_out, device=None):
+    def __init__(self, assignment, topo, placement, token_bytes, *, with_act_out, device=None, nodedup=False):
         self.P = topo.num_gpus
         self.a = assignment
         self.topo = topo
@@ -193,6 +193,7 @@ class _Session:
         self.cluster = EmulatedCluster(
             self.P, placement.num_experts, assignment.topk, token_bytes, max_t,
             owner=placement.owner, node_of=topo.node_table(), with_act_out=with_act_out, device=self.dev,
+            nodedup=nodedup,
         )
         self.idx = [torch.as_tensor(assignment.experts[i], dtype=torch.int64, device=self.dev).contiguous()
                     for i in self.ids]
@@ -252,20 +253,9 @@ class _Session:
 
 def _open_session(assignment, topo, placement, token_bytes, ablate, *, with_act_out, device=None) -> _Session:
     """A session whose ranks push without dedup when ``planner`` is ablated
-    (every (token, k) row crosses the link; FUSCO_NODEDUP is read at fs_create)."""
-    import os
-
-    if "planner" not in ablate:
-        return _Session(assignment, topo, placement, token_bytes, with_act_out=with_act_out, device=device)
-    prev = os.environ.get("FUSCO_NODEDUP")
-    os.environ["FUSCO_NODEDUP"] = "1"
-    try:
-        return _Session(assignment, topo, placement, token_bytes, with_act_out=with_act_out, device=device)
-    finally:
-        if prev is None:
-            os.environ.pop("FUSCO_NODEDUP", None)
-        else:
-            os.environ["FUSCO_NODEDUP"] = prev
+    (every (token, k) row crosses the link, ``fs_set_nodedup``)."""
+    return _Session(assignment, topo, placement, token_bytes, with_act_out=with_act_out, device=device,
+                    nodedup="planner" in ablate)
 
 
 def build_plan_pair(

@@ -491,6 +491,13 @@ long long fs_max_rows(fs_handle_t h) { return h ? h->max_rows : -1; }
 
 unsigned int fs_epoch(fs_handle_t h) { return h ? h->epoch : 0u; }
 
+int fs_set_nodedup(fs_handle_t h, int on) {
+  if (!h) return fail(FS_EINVAL, "null handle");
+  if (on != 0 && on != 1) return fail(FS_EINVAL, "on must be 0 or 1");
+  h->nodedup = on;
+  return FS_OK;
+}
+
 int fs_layout(fs_handle_t h, const void* topk_idx, int idx_bytes, int num_tokens, int32_t* row_of,
               int32_t* expert_counts, int32_t* expert_offsets, uint8_t* first_mask,
               uint32_t* rank_mask, int64_t* stats, int phase, void* stream) {

@@ -127,6 +127,7 @@ class Rank:
         with_act_out: bool,
         grid_ctas: int = 0,
         timeout_ms: int = 0,
+        nodedup: bool = False,
     ):
         self.device = torch.device(device)
         self.dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
@@ -147,6 +148,8 @@ class Rank:
             peers, int(grid_ctas), int(timeout_ms), byref(h),
         )
         self.handle = h
+        if nodedup:  # the reference's planner ablation: every (token, k) row crosses the link
+            call("fs_set_nodedup", h, 1)
         self.with_act_out = bool(with_act_out)
         self.max_rows = int(_lib.load().fs_max_rows(h))
         self.region = regions[rank]
@@ -302,6 +305,7 @@ class EmulatedCluster:
         grid_ctas: int = 0,
         device: torch.device | str | None = None,
         timeout_ms: int = 0,
+        nodedup: bool = False,
     ):
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         if self.device.index is None:
@@ -323,7 +327,7 @@ class EmulatedCluster:
                 device=self.device, rank=r, world=world, num_experts=num_experts, topk=topk,
                 token_bytes=token_bytes, max_tokens=max_tokens, owner=owner, node_of=node_of,
                 regions=self.regions, max_rows=mr, with_act_out=with_act_out, grid_ctas=grid_ctas,
-                timeout_ms=timeout_ms,
+                timeout_ms=timeout_ms, nodedup=nodedup,
             )
             for r in range(world)
         ]
