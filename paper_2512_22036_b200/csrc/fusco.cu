@@ -40,7 +40,7 @@ struct RegionLayout {
 RegionLayout region_layout(int world, int E, int tb, long long max_rows, int with_act_out) {
   RegionLayout L;
   L.off_count = kSigBytes;
-  L.count_stride = align256((size_t)world * E * sizeof(int32_t));
+  L.count_stride = align256((size_t)world * E * sizeof(uint64_t));  // epoch-tagged words
   L.off_fansrc = L.off_count + 2 * L.count_stride;
   L.fansrc_stride = align256((size_t)max_rows * sizeof(int32_t));
   L.off_act = L.off_fansrc + 2 * L.fansrc_stride;

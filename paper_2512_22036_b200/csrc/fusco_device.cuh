@@ -22,7 +22,7 @@ constexpr uint32_t kFull = 0xffffffffu;
 
 // Offsets inside the 4 KiB signal block at the start of every region.
 constexpr size_t kSigBytes = 4096;
-constexpr size_t kOffCountFlag = 0;    // u32[FS_MAX_RANKS]: layout counts published
+constexpr size_t kOffCountFlag = 0;    // u32[FS_MAX_RANKS]: reserved (the counts are epoch-tagged words)
 constexpr size_t kOffReadyFlag = 256;  // u32[FS_MAX_RANKS]: expert outputs ready
 constexpr size_t kOffArrive = 512;     // u32[FS_MAX_RANKS]: source s finished pushing here (epoch)
 constexpr size_t kOffDone = 1024;      // u64: reserved
@@ -86,6 +86,9 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ int ld_relaxed_sys_s32(const int32_t* p) {
   int v;
   asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -125,6 +128,46 @@ __device__ __forceinline__ bool wait_u64_geq(const unsigned long long* p, unsign
     }
   }
   return true;
+}
+
+// ---- count all-gather, epoch-tagged words ("LL") ---------------------------
+// Each word of the P x E count matrix carries (epoch << 32 | count): a reader
+// polls the words themselves, so the publisher needs neither a release fence
+// nor a separate flag (one NVLink traversal instead of data + fence + flag).
+__device__ __forceinline__ void publish_count(const FsArgs& a, int parity, uint32_t epoch, int e, int count) {
+  const unsigned long long w = ((unsigned long long)epoch << 32) | (uint32_t)count;
+  for (int g = 0; g < a.world; ++g) {
+    unsigned long long* m =
+        reinterpret_cast<unsigned long long*>(a.peer[g] + a.off_count + (size_t)parity * a.count_stride);
+    st_relaxed_sys_u64(m + (size_t)a.rank * a.E + e, w);
+  }
+}
+// Σ_q cnt[q][e] and Σ_{q<rank} cnt[q][e] from this rank's matrix, waiting for
+// every source's word of this epoch.
+__device__ __forceinline__ void gather_counts(const FsArgs& a, int parity, uint32_t epoch, int e, int* tot,
+                                              int* before) {
+  const unsigned long long* m =
+      reinterpret_cast<const unsigned long long*>(a.peer[a.rank] + a.off_count + (size_t)parity * a.count_stride);
+  int t = 0, b = 0;
+  for (int q = 0; q < a.world; ++q) {
+    const unsigned long long* p = m + (size_t)q * a.E + e;
+    unsigned long long w = ld_acquire_sys_u64(p);
+    if ((uint32_t)(w >> 32) != epoch) {
+      const unsigned long long t0 = globaltimer();
+      do {
+        if (globaltimer() - t0 > a.timeout_ns) {
+          record_error(a.status, FS_ETIMEOUT);
+          break;
+        }
+        w = ld_acquire_sys_u64(p);
+      } while ((uint32_t)(w >> 32) != epoch);
+    }
+    const int v = (int)(uint32_t)w;
+    t += v;
+    b += (q < a.rank) ? v : 0;
+  }
+  *tot = t;
+  *before = b;
 }
 
 // End of a rank's push phase: every CTA counts itself done on a local

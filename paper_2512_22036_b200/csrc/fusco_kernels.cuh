@@ -313,20 +313,14 @@ __global__ void __launch_bounds__(kLayoutThreads)
     trace_stamp(a, FS_TRACE_LAYOUT_GRIDSYNC);
 
     // One CTA publishes this rank's per-expert totals into every peer's count
-    // matrix row [s] (the P x E count all-gather, 8 KB at P=8, E=256), then
-    // one release store per peer.  A single rank needs no publication.
+    // matrix row [s] (the P x E count all-gather, 16 KB of epoch-tagged words
+    // at P=8, E=256).  A single rank needs no publication.
     if (blockIdx.x == 0) {
       int32_t* next_totals = a.totals + (size_t)(parity ^ 1) * E;
       long long* next_stats = a.stat_part + (parity ^ 1) * 8;
-      if (P > 1) {
-        for (int e = tid; e < E; e += kLayoutThreads) {
-          const int tot = single ? cnt_s[e] : ld_cg(totals + e);
-          for (int g = 0; g < P; ++g) {
-            int32_t* dst = reinterpret_cast<int32_t*>(a.peer[g] + a.off_count + (size_t)parity * a.count_stride);
-            dst[(size_t)s * E + e] = tot;
-          }
-        }
-      }
+      if (P > 1)
+        for (int e = tid; e < E; e += kLayoutThreads)
+          publish_count(a, parity, epoch, e, single ? cnt_s[e] : ld_cg(totals + e));
       for (int e = tid; e < E; e += kLayoutThreads) next_totals[e] = 0;
       if (stats && tid >= 5 && tid < FS_NSTATS) stats[tid] = 0;
       if (tid < 8) {
@@ -335,12 +329,6 @@ __global__ void __launch_bounds__(kLayoutThreads)
       }
       // every CTA read the old epoch before the grid barrier: safe to bump
       if (tid == 0) *a.epoch_ptr = epoch;
-      if (P > 1) {
-        __syncthreads();
-        // release: the count rows happen-before these stores (bar.sync + release)
-        if (tid < P)
-          st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[tid] + kOffCountFlag) + s, epoch);
-      }
       trace_stamp(a, FS_TRACE_LAYOUT_PUBLISH);
     }
   }
@@ -363,22 +351,8 @@ __global__ void __launch_bounds__(kLayoutThreads)
     __syncthreads();
     if (c_first < nchunks) chunk_prefix(a.chunk_cnt, c_first * E, E, pre);
     if (P > 1) {
-      if (tid < P)
-        wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffCountFlag) + tid, epoch, a);
-      __syncthreads();
+      for (int e = tid; e < E; e += kLayoutThreads) gather_counts(a, parity, epoch, e, tot + e, before + e);
       trace_stamp(a, FS_TRACE_LAYOUT_WAIT);
-      const int32_t* cnt =
-          reinterpret_cast<const int32_t*>(a.peer[s] + a.off_count + (size_t)parity * a.count_stride);
-      for (int e = tid; e < E; e += kLayoutThreads) {
-        int t = 0, b = 0;
-        for (int q = 0; q < P; ++q) {
-          const int val = ld_cg(cnt + (size_t)q * E + e);
-          t += val;
-          b += (q < s) ? val : 0;
-        }
-        tot[e] = t;
-        before[e] = b;
-      }
     } else if (one_e) {
       if (tid < E) {
         tot[tid] = tv;
@@ -595,13 +569,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   }
   __syncthreads();
   if (crank == 0) {
-    if (P > 1) {
-      for (int e = tid; e < E; e += kClusterThreads)
-        for (int g = 0; g < P; ++g) {
-          int32_t* dst = reinterpret_cast<int32_t*>(a.peer[g] + a.off_count + (size_t)parity * a.count_stride);
-          dst[(size_t)s * E + e] = tot[e];
-        }
-    }
+    if (P > 1)
+      for (int e = tid; e < E; e += kClusterThreads) publish_count(a, parity, epoch, e, tot[e]);
     if (stats && tid < 4) {
       long long acc = 0;
       for (int r = 0; r < CS; ++r) {
@@ -617,31 +586,15 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     if (stats && tid >= 5 && tid < FS_NSTATS) stats[tid] = 0;
     if (tid < 8) a.work[(size_t)(parity ^ 1) * 8 + tid] = 0ull;
     if (tid == 0) *a.epoch_ptr = epoch;  // every CTA read the old epoch before the cluster barrier
-    if (P > 1) {
-      __syncthreads();
-      if (tid < P)
-        st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[tid] + kOffCountFlag) + s, epoch);
-    }
     trace_stamp(a, FS_TRACE_LAYOUT_PUBLISH);
   }
 
   if (P > 1) {
-    if (tid < P)
-      wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffCountFlag) + tid, epoch, a);
+    // tot[] is overwritten with the all-source totals (the DSMEM values were
+    // this rank's own, already published above)
     __syncthreads();
+    for (int e = tid; e < E; e += kClusterThreads) gather_counts(a, parity, epoch, e, tot + e, before + e);
     trace_stamp(a, FS_TRACE_LAYOUT_WAIT);
-    const int32_t* cm =
-        reinterpret_cast<const int32_t*>(a.peer[s] + a.off_count + (size_t)parity * a.count_stride);
-    for (int e = tid; e < E; e += kClusterThreads) {
-      int t = 0, b = 0;
-      for (int q = 0; q < P; ++q) {
-        const int val = ld_cg(cm + (size_t)q * E + e);
-        t += val;
-        b += (q < s) ? val : 0;
-      }
-      tot[e] = t;
-      before[e] = b;
-    }
   } else {
     for (int e = tid; e < E; e += kClusterThreads) before[e] = 0;
   }
