@@ -66,8 +66,6 @@ struct fs_ctx {
   int pdl;              // 1: programmatic dependent launch planner -> dispatch (FUSCO_PDL=0 disables)
   int pdl_multi;        // 1: PDL for the cooperative P > 1 movers too (FUSCO_PDL_MULTI=0 disables)
   int nodedup;          // 1: no per-rank dedup on dispatch (FUSCO_NODEDUP=1; planner ablation)
-  int comb_minb4;       // warp combine, K <= 2: force 4 CTAs/SM (FUSCO_COMB_MINB4=1)
-  int comb_nopipe;      // K <= 2: plain warp combine instead of the pipelined one (FUSCO_COMB_NOPIPE=1)
   int cluster_layout;   // 1: single-cluster DSMEM planner usable (E <= 256, K <= 8)
   size_t cluster_smem;
   int combine_tma;      // 1: TMA combine engine (FUSCO_COMBINE=tma)
@@ -354,10 +352,6 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
     h->pdl = !(pd && std::string(pd) == "0");
     const char* pm = getenv("FUSCO_PDL_MULTI");
     h->pdl_multi = h->pdl && !(pm && std::string(pm) == "0");
-    const char* mb = getenv("FUSCO_COMB_MINB4");
-    h->comb_minb4 = mb && std::string(mb) == "1";
-    const char* np = getenv("FUSCO_COMB_NOPIPE");
-    h->comb_nopipe = np && std::string(np) == "1";
     const char* lm = getenv("FUSCO_LAYOUT");  // grid (default, measured faster) | cluster
     h->cluster_layout = (lm && std::string(lm) == "cluster") && num_experts <= kClusterMaxE && topk <= kClusterMaxK;
     h->cluster_smem = layout_cluster_smem_bytes(num_experts, topk);
@@ -622,7 +616,7 @@ int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes, const int32_t
     return launch_ex(fn, h->comb_grid, kCombThreads, h->comb_smem, stream, targs, true, h->pdl_multi);
   }
   // rows in flight per unit: min(K, 4) (no registers reserved for loads that never issue)
-  if (vec16 && h->K <= 2 && !h->comb_minb4 && !h->comb_nopipe) {
+  if (vec16 && h->K <= 2) {  // software-pipelined top-1/top-2 mover
     fn = bf ? (f64 ? (const void*)combine_k2_kernel<true, true> : (const void*)combine_k2_kernel<true, false>)
             : (f64 ? (const void*)combine_k2_kernel<false, true> : (const void*)combine_k2_kernel<false, false>);
     if (h->world == 1 && h->pdl) {  // no cross-CTA waits at P=1: PDL launch behind the dispatch
@@ -643,16 +637,9 @@ int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes, const int32_t
       FS_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
       return FS_OK;
     }
-  } else if (vec16) {
-    if (h->K <= 2 && h->comb_minb4)
-      fn = bf ? (f64 ? (const void*)combine_kernel<int4, true, true, 4, 2, 4> : (const void*)combine_kernel<int4, true, false, 4, 2, 4>)
-              : (f64 ? (const void*)combine_kernel<int4, false, true, 4, 2, 4> : (const void*)combine_kernel<int4, false, false, 4, 2, 4>);
-    else if (h->K <= 2)
-      fn = bf ? (f64 ? (const void*)combine_kernel<int4, true, true, 4, 2> : (const void*)combine_kernel<int4, true, false, 4, 2>)
-              : (f64 ? (const void*)combine_kernel<int4, false, true, 4, 2> : (const void*)combine_kernel<int4, false, false, 4, 2>);
-    else
-      fn = bf ? (f64 ? (const void*)combine_kernel<int4, true, true, 4, 4> : (const void*)combine_kernel<int4, true, false, 4, 4>)
-              : (f64 ? (const void*)combine_kernel<int4, false, true, 4, 4> : (const void*)combine_kernel<int4, false, false, 4, 4>);
+  } else if (vec16) {  // K > 2: four rows' 16-byte loads in flight per lane
+    fn = bf ? (f64 ? (const void*)combine_kernel<int4, true, true, 4, 4> : (const void*)combine_kernel<int4, true, false, 4, 4>)
+            : (f64 ? (const void*)combine_kernel<int4, false, true, 4, 4> : (const void*)combine_kernel<int4, false, false, 4, 4>);
   } else {
     fn = bf ? (f64 ? (const void*)combine_kernel<int, true, true, 8, 4> : (const void*)combine_kernel<int, true, false, 8, 4>)
             : (f64 ? (const void*)combine_kernel<int, false, true, 8, 4> : (const void*)combine_kernel<int, false, false, 8, 4>);

@@ -991,8 +991,8 @@ __device__ __forceinline__ uint32_t pack_out(double lo, double hi) {
 __device__ __forceinline__ uint32_t f32_bits(float v) { return __float_as_uint(v); }
 __device__ __forceinline__ uint32_t f32_bits(double v) { return __float_as_uint(__double2float_rn(v)); }
 
-template <typename V, bool BF16, bool ACC64, int U, int KG, int MINB = 2>
-__global__ void __launch_bounds__(kMoveThreads, MINB)
+template <typename V, bool BF16, bool ACC64, int U, int KG>
+__global__ void __launch_bounds__(kMoveThreads, 2)
     combine_kernel(FsArgs a, const void* __restrict__ idx, const int32_t* __restrict__ row_of,
                    const void* __restrict__ topk_w, int w64, V* __restrict__ out, int src_sel,
                    int phase) {
