@@ -490,3 +490,25 @@ def test_ragged_epochs_stress(engines):
                 assert np.array_equal(res["outs"][s], want), f"epoch {it} output/{s}"
     finally:
         cl.close()
+
+
+@pytest.mark.gpu
+def test_missing_peer_times_out_loudly():
+    """Failure detection: a rank whose peer never publishes its counts does not
+    hang — the bounded flag wait records FS_ETIMEOUT and fs_check raises."""
+    from paper_2512_22036_b200._lib import FS_ETIMEOUT, FS_PHASE_LOCAL, FS_PHASE_REMOTE, FuscoError
+    from paper_2512_22036_b200.engine import EmulatedCluster
+
+    P, E, K, T = 2, 8, 2, 64
+    cl = EmulatedCluster(P, E, K, 256, T, owner=np.arange(E) % P, timeout_ms=200)
+    try:
+        r0 = cl.ranks[0]
+        idx = torch.as_tensor(np.stack([np.arange(T) % E, (np.arange(T) + 1) % E], 1), device=cl.device)
+        plan = r0.new_plan(idx)
+        r0.layout(plan, FS_PHASE_LOCAL)
+        r0.layout(plan, FS_PHASE_REMOTE)  # rank 1 never ran: its count words never arrive
+        with pytest.raises(FuscoError) as ei:
+            r0.check()
+        assert ei.value.code == FS_ETIMEOUT
+    finally:
+        cl.close()
