@@ -41,6 +41,7 @@ _LAZY = {
     # GPU-side names (import torch + libfusco on first use)
     "run_exchange": "api",
     "execute_exchange": "api",
+    "run_baseline": "api",
     "build_plan_pair": "api",
     "build_plan": "api",
     "dispatch_loads": "api",

@@ -441,3 +441,14 @@ def _run_disaggregated(assignment, topo, placement, token_bytes, *, payload_seed
 
 # SPEC.md:396,405 names for the whole-cluster (emulated) execution
 execute_exchange = run_exchange
+
+
+def run_baseline(assignment, topo, placement, token_bytes, *, payload_seed: int = 0, mode: str = "analytic",
+                 cost=None, expert_fn=identity_expert, materialize: bool = True, dtype: str = "f32",
+                 acc: str = "f64", device=None) -> ExchangeResult:
+    """The disaggregated pack / all-to-all / unpack shuffle without dedup
+    (reference run_baseline, engine.py:552-625): same output bytes as
+    ``run_exchange``, every (token, k) row crosses, four rearrangement passes."""
+    return run_exchange(assignment, topo, placement, token_bytes, payload_seed=payload_seed, mode=mode, cost=cost,
+                        ablate=("dcomm", "planner"), expert_fn=expert_fn, materialize=materialize, dtype=dtype,
+                        acc=acc, device=device)

@@ -1,0 +1,115 @@
+"""The reference's acceptance criteria that concern the hot path
+(reference tests/test_acceptance.py), run on the GPU path.
+
+* criterion 1: lossless round trip over 200 random instances (cluster shapes
+  N, M in {1, 2, 4}, E <= 64, K <= 8, T <= 1024, all three traffic patterns),
+  fused and disaggregated baseline activations byte-identical, < 60 s;
+* criterion 2: dedup factor exact (fused ships 300·tb, baseline K·300·tb);
+* criterion 3: zero rearrangement bytes for fused, 4·T·K·tb for the baseline;
+* criterion 6 (measured form): fused round trip faster than the baseline;
+* criterion 8: benchmark matrix rows deterministic in every non-time field.
+"""
+
+import time
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sf():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    import paper_2512_22036_b200 as pkg
+    from paper_2512_22036_b200 import _lib
+
+    _lib.load()
+    return pkg
+
+
+def test_criterion_1_lossless_round_trip(sf):
+    gens = (sf.gen_realworld, sf.gen_single_node, sf.gen_imbalanced)
+    rng = np.random.default_rng(1001)
+    start = time.monotonic()
+    for i in range(200):
+        if i == 0:  # the degenerate cluster: one GPU, one expert, one pick
+            n = m = epg = topk = 1
+            num_tokens, tb = 16, 16
+        else:
+            n = int(rng.choice([1, 2, 4]))
+            m = int(rng.choice([1, 2, 4]))
+            epg = int(rng.integers(1, 64 // (n * m) + 1))
+            topk = int(rng.integers(1, min(8, epg * m) + 1))
+            num_tokens = 1024 if i % 20 == 0 else int(rng.integers(16, 513))
+            tb = 4 * int(rng.integers(2, 17))
+        topo = sf.ClusterTopology(num_nodes=n, gpus_per_node=m)
+        pl = sf.round_robin_placement(n * m * epg, topo)
+        a = gens[i % 3](num_tokens, topk, topo, pl, seed=int(rng.integers(1 << 30)))
+        fused = sf.run_exchange(a, topo, pl, tb, payload_seed=i)
+        base = sf.run_baseline(a, topo, pl, tb, payload_seed=i)
+        width = tb // 4
+        src = fused.payloads.view(np.float32).reshape(num_tokens, width)
+        for g in range(topo.num_gpus):
+            assert np.array_equal(base.activation(g), fused.activation(g)), (i, g)
+        for name, r in (("fused", fused), ("baseline", base)):
+            for s in range(topo.num_gpus):
+                ids = r.combine_plan.local_tokens[s]
+                out = r.output(s).view(np.float32).reshape(ids.size, width)
+                assert np.allclose(out, src[ids], rtol=1e-5, atol=1e-6), (i, name, s)
+    elapsed = time.monotonic() - start
+    assert elapsed < 60.0, f"round-trip sweep took {elapsed:.1f}s"
+
+
+def test_criterion_2_dedup_factor_exact(sf):
+    topo, pl = sf.preset("test")
+    tb = 128
+    for seed in range(20):
+        topk = 2 + seed % 3
+        a = sf.gen_single_node(300, topk, topo, pl, seed=seed, remote_only=True)
+        fused = sf.run_exchange(a, topo, pl, tb, materialize=False)
+        base = sf.run_baseline(a, topo, pl, tb, materialize=False)
+        assert fused.dispatch_report.inter_node_bytes == 300 * tb
+        assert base.dispatch_report.inter_node_bytes == topk * 300 * tb
+        assert sf.naive_inter_node_bytes(a, pl, topo, tb) == base.dispatch_report.inter_node_bytes
+        assert int(sf.dispatch_loads(a, pl, topo, tb).sum()) == 300 * tb
+
+
+def test_criterion_3_zero_rearrangement(sf):
+    topo, pl = sf.preset("test")
+    tb = 64
+    a = sf.gen_realworld(512, 4, topo, pl, seed=3)
+    fused = sf.run_exchange(a, topo, pl, tb, materialize=False)
+    base = sf.run_baseline(a, topo, pl, tb, materialize=False)
+    for rep in (fused.dispatch_report, fused.combine_report):
+        assert rep.rearrange_bytes == 0 and rep.rearrange_s == 0.0
+    assert base.dispatch_report.rearrange_bytes + base.combine_report.rearrange_bytes == 4 * 512 * 4 * tb
+
+
+def test_criterion_6_fused_faster_than_baseline(sf):
+    """Measured form of the ablation ordering: on the box8 shape the fused
+    round trip (graph-timed kernels) beats the disaggregated baseline."""
+    from paper_2512_22036_b200 import matrix as M
+
+    topo, pl = sf.preset("box8")
+    cfg = M.BenchConfig(topo, pl, ("realworld",), (4096,), topk=8, token_bytes=7168 * 2, repeats=1,
+                        variants=("fused", "baseline"))
+    rows = {r["variant"]: r for r in M.run_matrix(cfg)["rows"]}
+    assert rows["fused"]["total_s"] < rows["baseline"]["total_s"]
+    assert rows["fused"]["inter_node_bytes"] < rows["baseline"]["inter_node_bytes"]
+
+
+def test_criterion_8_matrix_deterministic(sf):
+    from paper_2512_22036_b200 import matrix as M
+
+    topo, pl = sf.preset("test")
+    cfg = M.BenchConfig(topo, pl, ("realworld", "imbalanced"), (256,), topk=4, token_bytes=64, repeats=1,
+                        variants=("fused", "planner_off"))
+    timing = {"preprocess_s", "rearrange_s", "communicate_s", "total_s", "latency_us", "routed_gbps", "hbm_gbps",
+              "roofline_frac"}
+    docs = [M.run_matrix(cfg) for _ in range(2)]
+    assert docs[0]["fingerprint"] == docs[1]["fingerprint"]
+    strip = lambda d: [{k: v for k, v in r.items() if k not in timing} for r in d["rows"]]  # noqa: E731
+    assert strip(docs[0]) == strip(docs[1])
