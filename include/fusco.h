@@ -91,7 +91,10 @@ extern "C" {
 #define FS_TRACE_COMBINE_BEGIN 12
 #define FS_TRACE_COMBINE_READY 13
 #define FS_TRACE_COMBINE_END 14
-#define FS_NTRACE 16
+#define FS_TRACE_LAYOUT_LAST 16   /* thread 0 of the last CTA to leave the kernel */
+#define FS_TRACE_DISPATCH_LAST 17
+#define FS_TRACE_COMBINE_LAST 18
+#define FS_NTRACE 24                /* slots 20-22: exit counters behind the *_LAST stamps */
 
 typedef struct fs_ctx* fs_handle_t;
 

@@ -71,6 +71,20 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 __device__ __forceinline__ void trace_stamp(const FsArgs& a, int slot) {
   if (a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) a.trace[slot] = globaltimer();
 }
+// Tracing only: stamps `slot` when thread 0 of the last CTA of the launch
+// leaves the kernel (any return path: a destructor), so the tail after CTA 0
+// is visible.  Counter slot = slot + 4; same grid size every launch assumed.
+struct TraceLast {
+  const FsArgs& a;
+  int slot;
+  __device__ TraceLast(const FsArgs& args, int s) : a(args), slot(s) {}
+  __device__ ~TraceLast() {
+    if (a.trace != nullptr && threadIdx.x == 0) {
+      const unsigned long long old = atomicAdd(a.trace + slot + 4, 1ull);
+      if ((old + 1) % gridDim.x == 0) a.trace[slot] = globaltimer();
+    }
+  }
+};
 
 __device__ __forceinline__ void record_error(int* status, int code) {
   atomicCAS(status, FS_OK, code);

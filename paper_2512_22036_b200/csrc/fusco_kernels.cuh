@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(kLayoutThreads)
                   uint8_t* __restrict__ first_mask, uint32_t* __restrict__ rank_mask,
                   long long* __restrict__ stats, int32_t* __restrict__ expert_counts,
                   int32_t* __restrict__ expert_offsets, int phase) {
+  TraceLast trace_last_(a, FS_TRACE_LAYOUT_LAST);
   extern __shared__ __align__(16) uint32_t sm[];
   __shared__ long long red[kLayoutWarps][4];
   __shared__ int rows_total;
@@ -744,6 +745,7 @@ template <typename V>
 __global__ void __launch_bounds__(kMoveThreads)
     dispatch_kernel(FsArgs a, const V* __restrict__ x, const void* __restrict__ idx,
                     const int32_t* __restrict__ row_of, int phase) {
+  TraceLast trace_last_(a, FS_TRACE_DISPATCH_LAST);
   constexpr int U = MoveCfg<V>::U;
   constexpr int SW = MoveCfg<V>::kSliceWords;
   const int K = a.K, T = a.T, P = a.world, s = a.rank;
@@ -854,6 +856,7 @@ template <int LAG>
 __global__ void __launch_bounds__(kTmaThreads)
     dispatch_tma_kernel(FsArgs a, const char* __restrict__ x, const void* __restrict__ idx,
                         const int32_t* __restrict__ row_of, int phase, int nslots) {
+  TraceLast trace_last_(a, FS_TRACE_DISPATCH_LAST);
   extern __shared__ __align__(128) char tsm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
   uint64_t* empty = full + kTmaMaxSlots;
@@ -996,6 +999,7 @@ __global__ void __launch_bounds__(kMoveThreads, 2)
     combine_kernel(FsArgs a, const void* __restrict__ idx, const int32_t* __restrict__ row_of,
                    const void* __restrict__ topk_w, int w64, V* __restrict__ out, int src_sel,
                    int phase) {
+  TraceLast trace_last_(a, FS_TRACE_COMBINE_LAST);
   using Acc = typename std::conditional<ACC64, double, float>::type;
   using EL = Elem<V, BF16>;
   // U vector words per lane per unit; KG experts' rows in flight together
@@ -1125,6 +1129,7 @@ template <bool BF16, bool ACC64>
 __global__ void __launch_bounds__(kMoveThreads)
     combine_k2_kernel(FsArgs a, const void* __restrict__ idx, const int32_t* __restrict__ row_of,
                       const void* __restrict__ topk_w, int w64, int4* __restrict__ out, int src_sel, int phase) {
+  TraceLast trace_last_(a, FS_TRACE_COMBINE_LAST);
   using Acc = typename std::conditional<ACC64, double, float>::type;
   using EL = Elem<int4, BF16>;
   constexpr int U = 4;
@@ -1297,6 +1302,7 @@ __global__ void __launch_bounds__(kCombThreads)
     combine_tma_kernel(FsArgs a, const void* __restrict__ idx, const int32_t* __restrict__ row_of,
                        const void* __restrict__ topk_w, int w64, char* __restrict__ out, int src_sel,
                        int phase, int nstages, int sb) {
+  TraceLast trace_last_(a, FS_TRACE_COMBINE_LAST);
   using Acc = typename std::conditional<ACC64, double, float>::type;
   using EL = Elem<int4, BF16>;
   extern __shared__ __align__(128) char csm[];

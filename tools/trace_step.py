@@ -39,7 +39,8 @@ idx = torch.as_tensor(a.experts[sel], device=dev)
 w = torch.as_tensor(a.weights[sel], dtype=torch.float32, device=dev)
 names = {0: "layout.begin", 6: "layout.staged", 7: "dispatch.signal", 1: "layout.hist", 15: "layout.totals", 2: "layout.gridsync", 3: "layout.publish", 4: "layout.wait",
          5: "layout.end", 8: "dispatch.begin", 9: "dispatch.pushed", 10: "dispatch.arrived", 11: "dispatch.end",
-         12: "combine.begin", 13: "combine.ready", 14: "combine.end"}
+         12: "combine.begin", 13: "combine.ready", 14: "combine.end", 16: "layout.last_cta_exit",
+         17: "dispatch.last_cta_exit", 18: "combine.last_cta_exit"}
 lib = _lib.load()
 for it in range(30):
     plan = buf.build_plan(idx)
@@ -74,7 +75,7 @@ if os.environ.get("TRACE_GRAPH") == "1":  # replay steps as one CUDA graph: no h
         g.replay()
     torch.cuda.synchronize()
     buf.check()
-tr = (ctypes.c_uint64 * 16)()
+tr = (ctypes.c_uint64 * 24)()
 _lib.call("fs_trace", buf.r.handle, tr, _lib.stream_ptr())
 t = np.array(list(tr), dtype=np.int64)
 lines = [f"[rank {rank}] {cfg} world={world}"]
