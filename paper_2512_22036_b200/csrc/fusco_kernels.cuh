@@ -1343,6 +1343,8 @@ __global__ void __launch_bounds__(kCombThreads)
   if (P > 1 && threadIdx.x < P)
     wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffReadyFlag) + threadIdx.x, epoch, a);
   __syncthreads();
+  // the rows the bulk copies (async proxy) read were published to generic-proxy acquires
+  if (P > 1 && threadIdx.x < 32) fence_proxy_async_global();
   trace_stamp(a, FS_TRACE_COMBINE_READY);
   const long long items = (long long)T * S;
 
