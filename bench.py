@@ -560,7 +560,7 @@ def main() -> int:
             "zipf_s": zipf,
             "expert": "identity (combine pulls the dispatched rows)",
             "combine_accumulate": "fp32",
-            "l2": f"inputs larger than L2: {NSET} rotating input/output sets + double-buffered activations, "
+            "l2": f"inputs larger than L2: {NSET} rotating input/output sets + the activation buffer, "
                   f"{(T_l * tb * 2 + int(tr['rows'].max()) * tb) / 2**20:.0f} MiB touched per step per rank",
             "value_def": "routed-row bytes (dispatch + combine, all ranks) / step time",
         },

@@ -45,7 +45,9 @@ RegionLayout region_layout(int world, int E, int tb, long long max_rows, int wit
   L.fansrc_stride = align256((size_t)max_rows * sizeof(int32_t));
   L.off_act = L.off_fansrc + 2 * L.fansrc_stride;
   L.act_stride = align256((size_t)max_rows * (size_t)tb);
-  L.off_actout = L.off_act + 2 * L.act_stride;
+  // one activation buffer: a rank's next dispatch cannot start before every
+  // rank has published the next epoch's counts, i.e. finished this combine
+  L.off_actout = L.off_act + L.act_stride;
   L.total = L.off_actout + (with_act_out ? L.act_stride : 0);
   return L;
 }
@@ -471,7 +473,7 @@ int fs_buffer_ptr(fs_handle_t h, int which, void** ptr_out) {
   if (!h || !ptr_out) return fail(FS_EINVAL, "null argument");
   char* base = h->peers[h->rank];
   if (which == 0) {
-    *ptr_out = base + h->L.off_act + (size_t)(h->epoch & 1u) * h->L.act_stride;
+    *ptr_out = base + h->L.off_act;  // fixed address: safe to capture in a CUDA graph
   } else if (which == 1) {
     if (!h->with_act_out) return fail(FS_EINVAL, "handle was created without an act_out buffer");
     *ptr_out = base + h->L.off_actout;

@@ -759,7 +759,7 @@ __global__ void __launch_bounds__(kMoveThreads)
   griddep_wait();  // row_of / the epoch come from the planner
   const uint32_t epoch = load_epoch(a);
   const int parity = (int)(epoch & 1u);
-  const size_t act_off = a.off_act + (size_t)parity * a.act_stride;
+  const size_t act_off = a.off_act;
   const size_t fan_off = a.off_fansrc + (size_t)parity * a.fansrc_stride;
   trace_stamp(a, FS_TRACE_DISPATCH_BEGIN);
 
@@ -885,7 +885,7 @@ __global__ void __launch_bounds__(kTmaThreads)
   griddep_wait();  // row_of / the epoch come from the planner
   const uint32_t epoch = load_epoch(a);
   const int parity = (int)(epoch & 1u);
-  const size_t act_off = a.off_act + (size_t)parity * a.act_stride;
+  const size_t act_off = a.off_act;
   const size_t fan_off = a.off_fansrc + (size_t)parity * a.fansrc_stride;
   trace_stamp(a, FS_TRACE_DISPATCH_BEGIN);
 
@@ -1014,7 +1014,7 @@ __global__ void __launch_bounds__(kMoveThreads, 2)
   griddep_wait();  // rows / the epoch from the previous kernel (PDL launch)
   const uint32_t epoch = load_epoch(a);
   const size_t src_off =
-      src_sel == FS_SRC_ACT_OUT ? a.off_actout : a.off_act + (size_t)(epoch & 1u) * a.act_stride;
+      src_sel == FS_SRC_ACT_OUT ? a.off_actout : a.off_act;
 
   trace_stamp(a, FS_TRACE_COMBINE_BEGIN);
   // "expert outputs ready" handshake: this rank's act/act_out rows were
@@ -1145,7 +1145,7 @@ __global__ void __launch_bounds__(kMoveThreads)
   griddep_wait();                 // dispatched rows / epoch from the previous kernel
   const uint32_t epoch = load_epoch(a);
   const size_t src_off =
-      src_sel == FS_SRC_ACT_OUT ? a.off_actout : a.off_act + (size_t)(epoch & 1u) * a.act_stride;
+      src_sel == FS_SRC_ACT_OUT ? a.off_actout : a.off_act;
   trace_stamp(a, FS_TRACE_COMBINE_BEGIN);
   if ((phase & FS_PHASE_LOCAL) && P > 1) {
     if (blockIdx.x == 0 && threadIdx.x < P)
@@ -1332,7 +1332,7 @@ __global__ void __launch_bounds__(kCombThreads)
   griddep_wait();  // dispatched rows / the epoch
   const uint32_t epoch = load_epoch(a);
   const size_t src_off =
-      src_sel == FS_SRC_ACT_OUT ? a.off_actout : a.off_act + (size_t)(epoch & 1u) * a.act_stride;
+      src_sel == FS_SRC_ACT_OUT ? a.off_actout : a.off_act;
   trace_stamp(a, FS_TRACE_COMBINE_BEGIN);
 
   if ((phase & FS_PHASE_LOCAL) && P > 1) {

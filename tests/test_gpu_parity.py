@@ -512,3 +512,40 @@ def test_missing_peer_times_out_loudly():
         assert ei.value.code == FS_ETIMEOUT
     finally:
         cl.close()
+
+
+@pytest.mark.gpu
+def test_cuda_graph_replay_with_captured_expert():
+    """A CUDA graph that captures planner, dispatch, an expert reading the
+    activation view, and combine replays correctly with fresh inputs every
+    replay: the activation buffer lives at a fixed address (it is not
+    double-buffered by epoch)."""
+    pkg = _pkg()
+    T, E, K, H = 256, 8, 2, 256
+    buf = pkg.EPBuffer(num_experts=E, topk=K, hidden=H, dtype="f32", max_tokens=T, with_act_out=True)
+    try:
+        dev = buf.device
+        topo = pkg.box(1)
+        a = pkg.gen_realworld(T, K, topo, pkg.round_robin_placement(E, topo), seed=5)
+        idx = torch.as_tensor(a.experts, device=dev)
+        w = torch.as_tensor(a.weights, dtype=torch.float64, device=dev)
+        x = torch.zeros((T, H), dtype=torch.float32, device=dev)
+        out = torch.empty_like(x)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                plan = buf.build_plan(idx)
+                act = buf.dispatch(x, plan)
+                buf.expert_out().copy_(act * 2.0)  # the "expert": a captured torch kernel reading act
+                buf.combine(plan, w, out, src="act_out", acc="f64")
+        torch.cuda.current_stream().wait_stream(side)
+        for it in range(4):
+            x.copy_(torch.randn((T, H), generator=torch.Generator(device=dev).manual_seed(it), device=dev))
+            g.replay()
+            torch.cuda.synchronize()
+            buf.check()
+            torch.testing.assert_close(out, 2.0 * x, rtol=1e-6, atol=1e-6)
+    finally:
+        buf.close()
