@@ -139,7 +139,7 @@ int fs_destroy(fs_handle_t h);
 /* Local experts (ascending id) and device pointers into the own region. */
 int fs_num_local_experts(fs_handle_t h, int* n_out);
 int fs_grid_ctas(fs_handle_t h, int* n_out);
-/* which: 0 = act of the current epoch, 1 = act_out */
+/* which: 0 = act, 1 = act_out (fixed addresses for the handle's lifetime) */
 int fs_buffer_ptr(fs_handle_t h, int which, void** ptr_out);
 long long fs_max_rows(fs_handle_t h);
 /* Current epoch (incremented by every fs_layout with the LOCAL phase). */
@@ -168,7 +168,9 @@ int fs_layout(fs_handle_t h, const void* topk_idx, int idx_bytes, int num_tokens
  * straight into every owner's expert-major activation rows, one NVLink
  * crossing per (token, destination rank); duplicates on the same rank are
  * fanned out receiver-side.  Output: this rank's act buffer rows
- * [0, expert_offsets[E_local]). */
+ * [0, expert_offsets[E_local]).  x must be complete before fs_layout of the
+ * same step is enqueued: the dispatch is launched as a programmatic
+ * dependent of the planner and may start streaming x in while it runs. */
 int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_bytes,
                 const int32_t* row_of, int num_tokens, int phase, void* stream);
 
