@@ -24,19 +24,22 @@ def main() -> int:
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     P, rank = dist.get_world_size(), dist.get_rank()
-    E, K, H, T_l = int(os.environ.get("MP_E", 64)), int(os.environ.get("MP_K", 8)), 2048, 256
+    E, K, T_l = int(os.environ.get("MP_E", 64)), int(os.environ.get("MP_K", 8)), 256
+    H = int(os.environ.get("MP_H", 2048))
+    dt = os.environ.get("MP_DT", "bf16")
     topo = box(P)
     pl = round_robin_placement(E, topo)
-    buf = EPBuffer(num_experts=E, topk=K, hidden=H, dtype="bf16", max_tokens=T_l, timeout_ms=20000)
+    buf = EPBuffer(num_experts=E, topk=K, hidden=H, dtype=dt, max_tokens=T_l, timeout_ms=20000)
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
     base = DisaggregatedShuffle(num_experts=E, topk=K)
     dev = torch.device("cuda", local)
     failures = 0
     for it in range(4):
         a = gen_realworld(P * T_l, K, topo, pl, seed=10 + it, zipf_s=0.4 * it)
         vals = np.random.default_rng(it).standard_normal((a.num_tokens, H)).astype(np.float32)
-        payload = O.encode(vals, "bf16")
+        payload = O.encode(vals, dt)
         ids = np.flatnonzero(a.source == rank)
-        x = torch.as_tensor(payload[ids], device=dev).view(torch.bfloat16).contiguous()
+        x = torch.as_tensor(payload[ids], device=dev).view(tdt).contiguous()
         idx = torch.as_tensor(a.experts[ids], device=dev)
         w = torch.as_tensor(a.weights[ids], dtype=torch.float64, device=dev)
         plan = buf.build_plan(idx)
@@ -57,7 +60,7 @@ def main() -> int:
         if not np.array_equal(plan.row_of.cpu().numpy(), row_of[ids]):
             print(f"[rank {rank}] iter {it}: row_of mismatch", flush=True)
             failures += 1
-        want = O.combine(acts, row_of, a.experts, a.weights, pl.owner, ids, "bf16")
+        want = O.combine(acts, row_of, a.experts, a.weights, pl.owner, ids, dt)
         if not np.array_equal(out.view(torch.uint8).cpu().numpy(), want):
             print(f"[rank {rank}] iter {it}: output mismatch", flush=True)
             failures += 1
@@ -67,8 +70,9 @@ def main() -> int:
             print(f"[rank {rank}] iter {it}: baseline activation differs from fused", flush=True)
             failures += 1
         bout = base.combine(bact, st, w.float())
-        ref = torch.as_tensor(O.decode(want, "bf16"), device=dev)
-        if not torch.allclose(bout.float(), ref, rtol=2.0**-8, atol=1e-3):
+        ref = torch.as_tensor(O.decode(want, dt), device=dev)
+        tol = dict(rtol=2.0**-8, atol=1e-3) if dt == "bf16" else dict(rtol=1e-5, atol=1e-6)
+        if not torch.allclose(bout.float(), ref, **tol):
             print(f"[rank {rank}] iter {it}: baseline output out of tolerance", flush=True)
             failures += 1
     t = torch.tensor([failures], device=dev)
