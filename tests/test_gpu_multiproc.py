@@ -22,20 +22,23 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("experts,topk,hidden,dtype", [
-    (64, 8, 2048, "bf16"),
-    (8, 2, 2048, "bf16"),
-    (32, 4, 1030, "bf16"),   # 2060-byte rows: not a multiple of 16, the 4-byte movers
-    (16, 4, 1024, "f32"),    # fp32 payload, f64-accumulate combine bit-exact
+@pytest.mark.parametrize("experts,topk,hidden,dtype,engines", [
+    (64, 8, 2048, "bf16", "auto:auto"),
+    (8, 2, 2048, "bf16", "auto:auto"),
+    (32, 4, 1030, "bf16", "auto:auto"),   # 2060-byte rows: not a multiple of 16, the 4-byte movers
+    (16, 4, 1024, "f32", "auto:auto"),    # fp32 payload, f64-accumulate combine bit-exact
+    (64, 8, 2048, "bf16", "tma:warp"),    # the other data movers across GPUs
 ])
-def test_multi_gpu_parity(experts, topk, hidden, dtype):
+def test_multi_gpu_parity(experts, topk, hidden, dtype, engines):
     n = torch.cuda.device_count() if torch.cuda.is_available() else 0
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     world = min(n, 8)
     if experts % world:
         pytest.skip("experts not divisible by world")
-    env = dict(os.environ, MP_E=str(experts), MP_K=str(topk), MP_H=str(hidden), MP_DT=dtype)
+    d, c = engines.split(":")
+    env = dict(os.environ, MP_E=str(experts), MP_K=str(topk), MP_H=str(hidden), MP_DT=dtype,
+               FUSCO_DISPATCH=d, FUSCO_COMBINE=c)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(ROOT / "tests" / "mp_worker.py")]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
