@@ -242,6 +242,9 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
   if (num_experts < 1 || num_experts > kMaxExperts) return fail(FS_EINVAL, "num_experts must be in [1, 1024]");
   if (topk < 1 || topk > 32 || topk > num_experts)
     return fail(FS_EINVAL, "topk must be in [1, min(32, num_experts)]");
+  // (token, slice) work units are indexed in 32 bits (smallest slice: 512 B)
+  if ((long long)max_tokens * (((long long)token_bytes + 511) / 512) >= (1ll << 31))
+    return fail(FS_EINVAL, "max_tokens x token_bytes too large for 32-bit work-unit indices");
   if (token_bytes <= 0 || token_bytes % 4)
     return fail(FS_EINVAL, "token_bytes must be a positive multiple of 4");
   if (max_tokens < 0) return fail(FS_EINVAL, "max_tokens must be >= 0");

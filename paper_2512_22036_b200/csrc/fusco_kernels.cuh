@@ -725,10 +725,11 @@ __device__ __forceinline__ void fan_out_rows(const FsArgs& a, size_t act_off, si
     }
   }
   cg::this_grid().sync();
-  const long long units = (long long)*reinterpret_cast<volatile unsigned long long*>(cnt) * S;
-  for (long long u = gw; u < units; u += nw) {
-    const int2 rf = __ldcg(a.fan_list + u / S);
-    const int w0 = (int)(u % S) * SW, rem = nv - w0;
+  const uint32_t units = (uint32_t)*reinterpret_cast<volatile unsigned long long*>(cnt) * (uint32_t)S;
+  for (uint32_t u = (uint32_t)gw; u < units; u += (uint32_t)nw) {
+    const uint32_t ri = u / (uint32_t)S;
+    const int2 rf = __ldcg(a.fan_list + ri);
+    const int w0 = (int)(u - ri * (uint32_t)S) * SW, rem = nv - w0;
     const V* src = act + (size_t)rf.y * nv + w0;
     V* dst = act + (size_t)rf.x * nv + w0;
     V v[U];
@@ -765,15 +766,16 @@ __global__ void __launch_bounds__(kMoveThreads)
 
   if (phase & FS_PHASE_LOCAL) {
     const long long units = (long long)T * S;
+    const uint32_t uS = (uint32_t)S;
     unsigned long long* ctr = work_ctr(a, epoch, kWorkDispatch);
     long long u = claim_warp(ctr);
-    KMeta nxt = u < units ? load_meta(a, idx, row_of, (int)(u / S), lane) : KMeta{0, -1};
+    KMeta nxt = u < units ? load_meta(a, idx, row_of, (int)((uint32_t)u / uS), lane) : KMeta{0, -1};
     while (u < units) {
-      const int i = (int)(u / S);
-      const int sl = (int)(u - (long long)i * S);
+      const int i = (int)((uint32_t)u / uS);
+      const int sl = (int)((uint32_t)u - (uint32_t)i * uS);
       const KMeta cur = nxt;
       const long long un = claim_warp(ctr);  // next unit: claimed and prefetched during this one
-      if (un < units) nxt = load_meta(a, idx, row_of, (int)(un / S), lane);
+      if (un < units) nxt = load_meta(a, idx, row_of, (int)((uint32_t)un / uS), lane);
       // payload loads first: they do not depend on the destinations
       const int w0 = sl * SW;
       const V* src = x + (size_t)i * nv + w0;
@@ -1034,23 +1036,23 @@ __global__ void __launch_bounds__(kMoveThreads, 2)
     trace_stamp(a, FS_TRACE_COMBINE_READY);
     __shared__ int32_t owner_sm[kMaxExperts];
     load_owner_table(a, owner_sm);
-    const long long units = (long long)T * S;
+    const uint32_t units = (uint32_t)T * (uint32_t)S, uS = (uint32_t)S;  // 32-bit unit arithmetic
     auto load_w = [&](int i) -> Acc {
       if (lane >= K) return (Acc)0;
       const size_t pos = (size_t)i * K + lane;
       return w64 ? (Acc)reinterpret_cast<const double*>(topk_w)[pos]
                  : (Acc)reinterpret_cast<const float*>(topk_w)[pos];
     };
-    long long u = gw;
-    KMeta nxt = u < units ? load_meta(a, idx, row_of, (int)(u / S), lane) : KMeta{0, 0};
-    Acc nxt_w = u < units ? load_w((int)(u / S)) : (Acc)0;
-    for (; u < units; u += nw) {
-      const int i = (int)(u / S);
-      const int sl = (int)(u - (long long)i * S);
+    uint32_t u = (uint32_t)gw;
+    KMeta nxt = u < units ? load_meta(a, idx, row_of, (int)(u / uS), lane) : KMeta{0, 0};
+    Acc nxt_w = u < units ? load_w((int)(u / uS)) : (Acc)0;
+    for (; u < units; u += (uint32_t)nw) {
+      const int i = (int)(u / uS);
+      const int sl = (int)(u - (uint32_t)i * uS);
       const KMeta cur = nxt;
       const Acc wk = nxt_w;
-      if (u + nw < units) {
-        const int inext = (int)((u + nw) / S);
+      if (u + (uint32_t)nw < units) {
+        const int inext = (int)((u + (uint32_t)nw) / uS);
         nxt = load_meta(a, idx, row_of, inext, lane);
         nxt_w = load_w(inext);
       }
@@ -1138,8 +1140,10 @@ __global__ void __launch_bounds__(kMoveThreads)
   const int nv = a.tb / 16;
   const int S = (nv + SW - 1) / SW;
   const int lane = threadIdx.x & 31;
-  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  // unit indices fit in 32 bits (fs_create bounds max_tokens x slices):
+  // 32-bit division, and the token of a unit is computed once
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   __shared__ int32_t owner_sm[kMaxExperts];
   load_owner_table(a, owner_sm);  // prologue (static table) before the PDL wait
   griddep_wait();                 // dispatched rows / epoch from the previous kernel
@@ -1158,25 +1162,27 @@ __global__ void __launch_bounds__(kMoveThreads)
     __syncthreads();
   }
   trace_stamp(a, FS_TRACE_COMBINE_READY);
-  const long long units = (long long)T * S;
+  const uint32_t units = (uint32_t)T * (uint32_t)S;
 
   struct Unit {
-    long long u;
+    uint32_t u;
+    int i;
     const int4* src[2];
     Acc w[2];
     int w0, rem;
   };
-  auto load_w = [&](long long uu) -> Acc {
+  auto load_w = [&](int i) -> Acc {
     if (lane >= K) return (Acc)0;
-    const size_t pos = (size_t)(uu / S) * K + lane;
+    const size_t pos = (size_t)i * K + lane;
     return w64 ? (Acc)reinterpret_cast<const double*>(topk_w)[pos]
                : (Acc)reinterpret_cast<const float*>(topk_w)[pos];
   };
   // metadata (lanes 0..K-1) -> per-unit row pointers, broadcast to the warp
-  auto resolve = [&](long long uu, const KMeta& m, Acc wl) -> Unit {
+  auto resolve = [&](uint32_t uu, const KMeta& m, Acc wl) -> Unit {
     Unit x;
     x.u = uu;
-    const int i = (int)(uu / S), sl = (int)(uu - (long long)i * S);
+    x.i = (int)(uu / (uint32_t)S);
+    const int sl = (int)(uu - (uint32_t)x.i * (uint32_t)S);
     x.w0 = sl * SW;
     x.rem = nv - x.w0;
     int g = 0, r = 0;
@@ -1191,7 +1197,6 @@ __global__ void __launch_bounds__(kMoveThreads)
       x.w[k] = __shfl_sync(kFull, wl, k);
       x.src[k] = reinterpret_cast<const int4*>(a.peer[gk] + src_off) + (size_t)rk * nv + x.w0;
     }
-    (void)i;
     return x;
   };
   auto issue = [&](const Unit& x, int4 (&v)[2][U]) {
@@ -1204,8 +1209,7 @@ __global__ void __launch_bounds__(kMoveThreads)
       }
   };
   auto finish = [&](const Unit& x, const int4 (&v)[2][U]) {
-    const int i = (int)(x.u / S);
-    int4* dst = out + (size_t)i * nv + x.w0;
+    int4* dst = out + (size_t)x.i * nv + x.w0;
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       const int w = j * 32 + lane;
@@ -1229,26 +1233,28 @@ __global__ void __launch_bounds__(kMoveThreads)
     }
   };
 
-  long long u = gw;
+  const uint32_t u = gw;
   if (u >= units) return;
-  KMeta m_next = load_meta(a, idx, row_of, (int)(u / S), lane);
-  Acc w_next = load_w(u);
+  KMeta m_next = load_meta(a, idx, row_of, (int)(u / (uint32_t)S), lane);
+  Acc w_next = load_w((int)(u / (uint32_t)S));
   Unit cur = resolve(u, m_next, w_next);
   if (u + nw < units) {
-    m_next = load_meta(a, idx, row_of, (int)((u + nw) / S), lane);
-    w_next = load_w(u + nw);
+    const int i1 = (int)((u + nw) / (uint32_t)S);
+    m_next = load_meta(a, idx, row_of, i1, lane);
+    w_next = load_w(i1);
   }
   int4 va[2][U], vb[2][U];
   issue(cur, va);
   for (;;) {
     // ---- cur in va; next goes to vb
-    const long long u1 = cur.u + nw;
+    const uint32_t u1 = cur.u + nw;
     Unit nxt;
     if (u1 < units) {
       nxt = resolve(u1, m_next, w_next);
       if (u1 + nw < units) {
-        m_next = load_meta(a, idx, row_of, (int)((u1 + nw) / S), lane);
-        w_next = load_w(u1 + nw);
+        const int in = (int)((u1 + nw) / (uint32_t)S);
+        m_next = load_meta(a, idx, row_of, in, lane);
+        w_next = load_w(in);
       }
       issue(nxt, vb);
     }
@@ -1256,12 +1262,13 @@ __global__ void __launch_bounds__(kMoveThreads)
     if (u1 >= units) break;
     cur = nxt;
     // ---- cur in vb; next goes to va
-    const long long u2 = cur.u + nw;
+    const uint32_t u2 = cur.u + nw;
     if (u2 < units) {
       nxt = resolve(u2, m_next, w_next);
       if (u2 + nw < units) {
-        m_next = load_meta(a, idx, row_of, (int)((u2 + nw) / S), lane);
-        w_next = load_w(u2 + nw);
+        const int in = (int)((u2 + nw) / (uint32_t)S);
+        m_next = load_meta(a, idx, row_of, in, lane);
+        w_next = load_w(in);
       }
       issue(nxt, va);
     }
@@ -1352,12 +1359,12 @@ __global__ void __launch_bounds__(kCombThreads)
     unsigned long long* ctr = work_ctr(a, epoch, kWorkCombine);
     auto load_w = [&](long long uu) -> Acc {
       if (lane >= K) return (Acc)0;
-      const size_t pos = (size_t)(uu / S) * K + lane;
+      const size_t pos = (size_t)((uint32_t)uu / (uint32_t)S) * K + lane;
       return w64 ? (Acc)reinterpret_cast<const double*>(topk_w)[pos]
                  : (Acc)reinterpret_cast<const float*>(topk_w)[pos];
     };
     long long u = claim_warp(ctr);
-    KMeta m = u < items ? load_meta(a, idx, row_of, (int)(u / S), lane) : KMeta{0, 0};
+    KMeta m = u < items ? load_meta(a, idx, row_of, (int)((uint32_t)u / (uint32_t)S), lane) : KMeta{0, 0};
     Acc wl = u < items ? load_w(u) : (Acc)0;
     int n = 0;
     for (;; ++n) {
@@ -1374,10 +1381,10 @@ __global__ void __launch_bounds__(kCombThreads)
       KMeta mn = KMeta{0, 0};
       Acc wn = (Acc)0;
       if (un < items) {
-        mn = load_meta(a, idx, row_of, (int)(un / S), lane);
+        mn = load_meta(a, idx, row_of, (int)((uint32_t)un / (uint32_t)S), lane);
         wn = load_w(un);
       }
-      const int i = (int)(u / S), j = (int)(u - (long long)i * S);
+      const int i = (int)((uint32_t)u / (uint32_t)S), j = (int)((uint32_t)u - (uint32_t)i * (uint32_t)S);
       (void)i;
       const int off = j * sb;
       const int len = min(sb, tb - off);
@@ -1405,7 +1412,7 @@ __global__ void __launch_bounds__(kCombThreads)
       mbar_wait(&full[q], (n / nstages) & 1);
       const long long u = slot_item[q];
       if (u < 0) break;
-      const int i = (int)(u / S), j = (int)(u - (long long)i * S);
+      const int i = (int)((uint32_t)u / (uint32_t)S), j = (int)((uint32_t)u - (uint32_t)i * (uint32_t)S);
       const int off = j * sb;
       const int nv = min(sb, tb - off) / 16;
       const char* st = stages + (size_t)q * stage_bytes;
