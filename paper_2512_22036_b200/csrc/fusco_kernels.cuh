@@ -152,7 +152,9 @@ __global__ void __launch_bounds__(kLayoutThreads)
   const uint32_t epoch = load_epoch(a) + ((phase & FS_PHASE_LOCAL) ? 1u : 0u);
   const int parity = (int)(epoch & 1u);
   trace_stamp(a, FS_TRACE_LAYOUT_BEGIN);
-  griddep_launch_dependents();  // the dispatch may start its row prefetch now
+  // the dispatch may start its row prefetch now (measured: triggering after the
+  // histogram instead, to spare the planner's loads the contention, is slower)
+  griddep_launch_dependents();
 
   __shared__ int warp_tot[kLayoutWarps];
   int32_t* owner_s = reinterpret_cast<int32_t*>(sm);
@@ -372,6 +374,7 @@ __global__ void __launch_bounds__(kLayoutThreads)
     block_segmented_base<kLayoutThreads>(E, tot, perm_s, seg_s, owner_s, ex_s, base, warp_tot);
     if (tid == 0) rows_total = ex_s[seg_s[s + 1]] - ex_s[seg_s[s]];
     __syncthreads();
+    trace_stamp(a, 19);
     for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
       if (c != c_first) {  // later chunks of this CTA (T > grid * 256)
         __syncthreads();
@@ -382,6 +385,7 @@ __global__ void __launch_bounds__(kLayoutThreads)
       }
       for (int e = tid; e < E; e += kLayoutThreads) pre[e] += base[e] + before[e];
       __syncthreads();
+      trace_stamp(a, 23);
       const int t0 = c * kLayoutThreads;
       const int nel = min(kLayoutThreads, T - t0) * K;
       const size_t base_el = (size_t)t0 * K;

@@ -39,7 +39,7 @@ idx = torch.as_tensor(a.experts[sel], device=dev)
 w = torch.as_tensor(a.weights[sel], dtype=torch.float32, device=dev)
 names = {0: "layout.begin", 6: "layout.staged", 7: "dispatch.signal", 1: "layout.hist", 15: "layout.totals", 2: "layout.gridsync", 3: "layout.publish", 4: "layout.wait",
          5: "layout.end", 8: "dispatch.begin", 9: "dispatch.pushed", 10: "dispatch.arrived", 11: "dispatch.end",
-         12: "combine.begin", 13: "combine.ready", 14: "combine.end", 16: "layout.last_cta_exit",
+         12: "combine.begin", 13: "combine.ready", 14: "combine.end", 16: "layout.last_cta_exit", 19: "layout.scanned", 23: "layout.pre",
          17: "dispatch.last_cta_exit", 18: "combine.last_cta_exit"}
 lib = _lib.load()
 for it in range(30):
