@@ -128,8 +128,12 @@ def test_library_validates_before_touching_cuda():
 
     n = c_size_t()
     _lib.call("fs_region_bytes", 8, 256, 14336, 1000, 1, byref(n))
-    # signal block + 2x counts + 2x fan_src + 3x rows
-    assert n.value >= 4096 + 3 * 1000 * 14336
+    # signal block + 2 parity copies of the epoch-tagged count words (u64 P x E)
+    # + 2 of fan_src (int32 per row) + the activation rows + the expert-output rows
+    a256 = lambda b: (b + 255) // 256 * 256  # noqa: E731
+    assert n.value == 4096 + 2 * a256(8 * 256 * 8) + 2 * a256(1000 * 4) + 2 * a256(1000 * 14336)
+    _lib.call("fs_region_bytes", 8, 256, 14336, 1000, 0, byref(n))
+    assert n.value == 4096 + 2 * a256(8 * 256 * 8) + 2 * a256(1000 * 4) + a256(1000 * 14336)
     with pytest.raises(ValueError):
         _lib.call("fs_region_bytes", 0, 256, 14336, 1000, 1, byref(n))
     owner = (np.arange(8) % 2).astype(np.int32)
