@@ -335,3 +335,23 @@ def test_plan_json_executes_to_reference_bytes(name):
             out = out + g["weights"][ids, k : k + 1] * stg[:, k]
         want = O.combine(acts, row_of, g["experts"], g["weights"], g["owner"], ids, "f32")
         assert np.array_equal(O.encode(out.astype(np.float32), "f32"), want)
+
+
+def test_header_constants_and_signatures_match_binding():
+    """include/fusco.h is the contract: every FS_* constant the Python binding
+    mirrors has the header's value, and every ctypes signature has the
+    prototype's parameter count."""
+    from paper_2512_22036_b200 import _lib
+
+    text = HEADER.read_text()
+    defines = dict(re.findall(r"#define\s+(FS_[A-Z0-9_]+)\s+\(?(-?\d+)\)?", text))
+    checked = 0
+    for name, val in vars(_lib).items():
+        if name.startswith("FS_") and isinstance(val, int) and name in defines:
+            assert val == int(defines[name]), name
+            checked += 1
+    assert checked >= 10
+    body = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    for name, params in re.findall(r"\b(fs_[a-z0-9_]+)\s*\(([^)]*)\)\s*;", body, flags=re.S):
+        n = 0 if params.strip() in ("", "void") else params.count(",") + 1
+        assert len(_lib.SIGNATURES[name][1]) == n, name
