@@ -113,3 +113,33 @@ def test_criterion_8_matrix_deterministic(sf):
     assert docs[0]["fingerprint"] == docs[1]["fingerprint"]
     strip = lambda d: [{k: v for k, v in r.items() if k not in timing} for r in d["rows"]]  # noqa: E731
     assert strip(docs[0]) == strip(docs[1])
+
+
+def test_odd_rank_counts_and_odd_rows_bit_exact(sf):
+    """Rank counts that are not powers of two (3, 5, 6, 7), random expert
+    counts / top-k / token sizes (4-byte multiples, some not 16-byte aligned)
+    and ragged per-rank batches: activations and f64-accumulated outputs
+    bit-identical to the reference restatement."""
+    from oracle import shuffle_oracle as O
+
+    rng = np.random.default_rng(77)
+    for i in range(24):
+        P = int(rng.choice([3, 5, 6, 7]))
+        E = P * int(rng.integers(1, 9))
+        K = int(rng.integers(1, min(8, E) + 1))
+        tb = 4 * int(rng.integers(1, 129))
+        topo = sf.box(P)
+        pl = sf.round_robin_placement(E, topo)
+        T = int(rng.integers(P, 64 * P))
+        a0 = sf.gen_realworld(T, K, topo, pl, seed=int(rng.integers(1 << 30)), zipf_s=float(rng.uniform(0, 1.5)))
+        source = np.sort(rng.integers(0, P, size=T))  # ragged ranks, some possibly empty
+        a = sf.RoutingAssignment(T, K, a0.experts, a0.weights, source)
+        r = sf.run_exchange(a, topo, pl, tb, payload_seed=i)
+        layouts, row_of = O.activation_layouts(a.experts, a.source, pl.owner, P)
+        acts = O.dispatch(r.payloads, layouts)
+        for g in range(P):
+            assert np.array_equal(r.activation(g).reshape(-1, tb), acts[g]), (i, g)
+        for s in range(P):
+            ids = np.flatnonzero(a.source == s)
+            want = O.combine(acts, row_of, a.experts, a.weights, pl.owner, ids, "f32")
+            assert np.array_equal(r.output(s).reshape(-1, tb), want), (i, s)
