@@ -398,7 +398,7 @@ class EPBuffer:
                        max_tokens=4096)
         plan = buf.build_plan(topk_idx)            # on-device layout planner
         act = buf.dispatch(x, plan)                # [rows, hidden], expert-major
-        y = buf.expert_out(plan)                   # write expert outputs here ...
+        y = buf.expert_out(plan.num_rows)          # write expert outputs here ...
         out = buf.combine(plan, topk_w)            # ... or pass src="act"
     """
 
@@ -439,26 +439,33 @@ class EPBuffer:
                tuple(int(o) for o in owner), int(grid_ctas))
         own = c_void_p()
         call("fs_sym_alloc", self.device.index, nbytes, byref(own))
-        handle = (ctypes.c_uint8 * 64)()
-        call("fs_ipc_handle", self.device.index, own, handle)
-        infos = bootstrap_exchange(bytes(handle), cfg, self.rank_id, group, exchange)
         self._peers = _Peers()
-        for g, h in enumerate(infos):
-            if g == self.rank_id:
-                self._peers.regions.append(own.value)
-                continue
-            p = c_void_p()
-            raw = (ctypes.c_uint8 * 64).from_buffer_copy(h)
-            call("fs_ipc_open", self.device.index, raw, byref(p))
-            self._peers.regions.append(p.value)
-            self._peers.opened.append(p.value)
+        try:
+            handle = (ctypes.c_uint8 * 64)()
+            call("fs_ipc_handle", self.device.index, own, handle)
+            infos = bootstrap_exchange(bytes(handle), cfg, self.rank_id, group, exchange)
+            for g, h in enumerate(infos):
+                if g == self.rank_id:
+                    self._peers.regions.append(own.value)
+                    continue
+                p = c_void_p()
+                raw = (ctypes.c_uint8 * 64).from_buffer_copy(h)
+                call("fs_ipc_open", self.device.index, raw, byref(p))
+                self._peers.regions.append(p.value)
+                self._peers.opened.append(p.value)
+            self.r = Rank(
+                device=self.device, rank=self.rank_id, world=self.world, num_experts=num_experts, topk=topk,
+                token_bytes=token_bytes, max_tokens=max_tokens, owner=owner, node_of=None,
+                regions=self._peers.regions, max_rows=mr, with_act_out=with_act_out, grid_ctas=grid_ctas,
+                timeout_ms=timeout_ms,
+            )
+        except BaseException:  # release what was mapped / allocated before re-raising
+            lib = _lib.load()
+            for p in self._peers.opened:
+                lib.fs_ipc_close(self.device.index, c_void_p(p))
+            lib.fs_sym_free(self.device.index, own)
+            raise
         self._own = own.value
-        self.r = Rank(
-            device=self.device, rank=self.rank_id, world=self.world, num_experts=num_experts, topk=topk,
-            token_bytes=token_bytes, max_tokens=max_tokens, owner=owner, node_of=None,
-            regions=self._peers.regions, max_rows=mr, with_act_out=with_act_out, grid_ctas=grid_ctas,
-            timeout_ms=timeout_ms,
-        )
         self.with_act_out = with_act_out
         self._closed = False
 
@@ -495,7 +502,7 @@ class EPBuffer:
         self.r.check(stream)
 
     def close(self) -> None:
-        if self._closed:
+        if getattr(self, "_closed", True):
             return
         self._closed = True
         self.r.close()
@@ -503,6 +510,18 @@ class EPBuffer:
         for p in self._peers.opened:
             lib.fs_ipc_close(self.device.index, c_void_p(p))
         lib.fs_sym_free(self.device.index, c_void_p(self._own))
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def bootstrap_exchange(handle: bytes, cfg: tuple, rank: int, group=None, exchange=None) -> list[bytes]:
