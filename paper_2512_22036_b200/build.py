@@ -19,7 +19,7 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB = LIB_DIR / "libfusco.so"
 SOURCES = [CSRC / "fusco.cu"]
-DEPS = SOURCES + [CSRC / "fusco_kernels.cuh", CSRC / "fusco_device.cuh", ROOT / "include" / "fusco.h"]
+DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "fusco.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

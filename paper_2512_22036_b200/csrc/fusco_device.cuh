@@ -21,6 +21,7 @@ namespace fusco {
 constexpr uint32_t kFull = 0xffffffffu;
 
 // Offsets inside the 4 KiB signal block at the start of every region.
+constexpr int kMoveThreads = 256;  // dispatch / combine warp-mover CTA size
 constexpr size_t kSigBytes = 4096;
 constexpr size_t kOffCountFlag = 0;    // u32[FS_MAX_RANKS]: reserved (the counts are epoch-tagged words)
 constexpr size_t kOffReadyFlag = 256;  // u32[FS_MAX_RANKS]: expert outputs ready
