@@ -56,6 +56,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         "-v" if verbose else "-O3",
         "-I",
         str(ROOT / "include"),
+        *os.environ.get("FUSCO_NVCC_FLAGS", "").split(),  # experiment hook, e.g. -DFUSCO_LD256
         "-o",
         str(tmp),
         *map(str, SOURCES),
