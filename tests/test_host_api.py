@@ -355,3 +355,30 @@ def test_header_constants_and_signatures_match_binding():
     for name, params in re.findall(r"\b(fs_[a-z0-9_]+)\s*\(([^)]*)\)\s*;", body, flags=re.S):
         n = 0 if params.strip() in ("", "void") else params.count(",") + 1
         assert len(_lib.SIGNATURES[name][1]) == n, name
+
+
+@pytest.mark.parametrize("cfg,P,want", [
+    ("mixtral", 2, (50.3, 50.7, 64.1, 64.4)),
+    ("mixtral", 8, (112.0, 113.2, 112.0, 113.2)),
+    ("qwen3", 8, (74.9, 75.2, 112.1, 113.1)),
+    ("dsv3", 8, (259.2, 261.8, 391.7, 396.4)),
+    ("dsv3_decode", 8, (8.1, 8.5, 12.3, 13.0)),
+    ("dsv3_zipf", 4, (154.7, 167.5, 336.0, 484.7)),
+])
+def test_bench_traffic_matches_reference_volumes(cfg, P, want):
+    """The NVLink byte accounting behind every multi-GPU roofline (bench.traffic)
+    reproduces SURVEY.md §8d's table, computed from the reference's own plans
+    (MiB: dispatch mean egress, dispatch max(eg, in), combine mean egress,
+    combine max(eg, in)); the dispatch egress equals dispatch_loads."""
+    import bench
+    from oracle import shuffle_oracle as O
+
+    hidden, dtype, E, K, T_l, _, _ = bench.CONFIGS[cfg]
+    a, pl = bench.routing_for(cfg, P, 0)
+    tb = hidden * (2 if dtype == "bf16" else 4)
+    tr = bench.traffic(a.experts, a.source, pl.owner, P, tb, T_l)
+    M = 2**20
+    got = (tr["d_eg"].mean() / M, np.maximum(tr["d_eg"], tr["d_in"]).max() / M,
+           tr["c_eg"].mean() / M, np.maximum(tr["c_eg"], tr["c_in"]).max() / M)
+    assert np.allclose(got, want, atol=0.051), got
+    assert np.array_equal(tr["d_eg"], O.dispatch_loads(a.experts, a.source, pl.owner, P, tb, 1))
