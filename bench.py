@@ -51,7 +51,9 @@ CONFIGS = {
     # diagnostic: top-1, so dispatch push bytes == combine pull bytes (no dedup, no fan-out)
     "k1": (7168, "bf16", 8, 1, 8192, 0.0, "diagnostic: hidden 7168 bf16, 8 experts top-1, 8192 tokens/rank"),
 }
-DEFAULT_CONFIG = "mixtral"  # BASELINE.json configs[1]
+# BASELINE.json configs[4]: the 1-8 GPU sweep config, and the largest one that
+# BASELINE.json defines at one GPU (the driver's N=1 line and its SCALE sweep)
+DEFAULT_CONFIG = "dsv3_zipf"
 
 NVLINK_NOMINAL = 900.0   # GB/s per direction per GPU (NVLink 5)
 NVLINK_MEASURED = 770.0  # GB/s peer copy, B200_PROFILING.md
@@ -175,6 +177,29 @@ def routing_for(cfg_name: str, P: int, seed: int):
     return a, pl
 
 
+def config_dict(cfg_name: str, P: int, rows_max: int | None = None, nset: int = 2) -> dict:
+    """The ``config`` object of the JSON line — identical for both arms."""
+    hidden, dtype, E, K, T_l, zipf, desc = CONFIGS[cfg_name]
+    tb = hidden * (2 if dtype == "bf16" else 4)
+    cfg = {
+        "workload": desc,
+        "name": cfg_name,
+        "ep": P,
+        "tokens_per_rank": T_l,
+        "hidden": hidden,
+        "experts": E,
+        "topk": K,
+        "zipf_s": zipf,
+        "expert": "identity (combine pulls the dispatched rows)",
+        "combine_accumulate": "fp32",
+        "value_def": "routed-row bytes (dispatch + combine, all ranks) / step time",
+    }
+    if rows_max is not None:
+        cfg["l2"] = (f"inputs larger than L2: {nset} rotating input/output sets + the activation buffer, "
+                     f"{(T_l * tb * 2 + rows_max * tb) / 2**20:.0f} MiB touched per step per rank")
+    return cfg
+
+
 def cpu_reference(cfg_name: str, P: int, seed: int, steps: int, warmup: int, budget_s: float = 150.0):
     """Reference CPU path (oracle port) on a bounded sample of the workload."""
     from oracle.cpu_baseline import shuffle_times
@@ -281,11 +306,13 @@ def main() -> int:
         if rank != 0:
             return 0
         cb = cpu_reference(args.config, world, args.seed, args.steps, args.warmup)
+        a_, pl_ = routing_for(args.config, world, args.seed)
+        tr_ = traffic(a_.experts, a_.source, pl_.owner, world, hidden * (2 if dtype == "bf16" else 4), T_l)
         line = {
             "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": cb["unit"], "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["latency_s"] * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
-            "data": "synthetic", "config": {"workload": desc, "ep": world},
+            "data": "synthetic", "config": config_dict(args.config, world, int(tr_["rows"].max())),
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }
@@ -409,7 +436,17 @@ def main() -> int:
         comb_args = [c[:-1] + (stream,) for c in comb_args]
         for _ in range(3):
             graph.replay()
+    nvc, nvc_err = None, None
+    if P > 1:  # NVLink data counters around the timed region (ncu cannot wrap a multi-rank run)
+        try:
+            from paper_2512_22036_b200.nvlink import NvlinkCounters
+
+            nvc = NvlinkCounters(dev)
+            nvc.read()
+        except Exception as e:  # measurement only: report why it is missing
+            nvc, nvc_err = None, repr(e)
     barrier()
+    link0 = nvc.read() if nvc else None
     host0 = time.perf_counter()
     start.record()
     if graph is not None:
@@ -423,8 +460,23 @@ def main() -> int:
     end.record()
     host_ms = (time.perf_counter() - host0) * 1e3
     barrier()
+    link1 = nvc.read() if nvc else None
     buf.check()
     total_ms = start.elapsed_time(end)
+    link_disp = None
+    if nvc:  # the same K steps without the combine: the dispatch's (and planner's) own link bytes
+        for i in range(args.steps):
+            f_layout(*lay_args)
+            f_disp(*disp_args[i % NSET])
+        barrier()
+        d0 = nvc.read()
+        for i in range(args.steps):
+            f_layout(*lay_args)
+            f_disp(*disp_args[i % NSET])
+        barrier()
+        d1 = nvc.read()
+        buf.check()
+        link_disp = (d1[0] - d0[0], d1[1] - d0[1])
     if graph is not None:  # per-kernel split from an eager pass of the same K steps
         barrier()
         for i in range(args.steps):
@@ -501,8 +553,14 @@ def main() -> int:
 
     vec = torch.tensor([total_ms, k_layout, k_disp, k_comb, e2e["ms"] if e2e else 0.0], dtype=torch.float64,
                        device=dev)
+    links = None
     if world > 1:
         dist.all_reduce(vec, op=dist.ReduceOp.MAX)
+        lk = torch.tensor([float(link1[0] - link0[0]), float(link1[1] - link0[1]), float(link_disp[0]),
+                           float(link_disp[1])] if nvc else [-1.0] * 4, dtype=torch.float64, device=dev)
+        allk = [torch.empty_like(lk) for _ in range(world)]
+        dist.all_gather(allk, lk)
+        links = torch.stack(allk).cpu().numpy() / args.steps  # [P, 4] bytes per step
     total_ms, k_layout, k_disp, k_comb, e2e_ms = vec.tolist()
     ms = total_ms / args.steps
     routed = 2.0 * P * T_l * K * tb  # bytes per step, whole job
@@ -533,9 +591,38 @@ def main() -> int:
                 "frac_of_nominal_900": achieved / NVLINK_NOMINAL,
                 "bytes_per_launch": b, "traffic": None}
     traffic_file = ROOT / "profiles" / "ncu_traffic.json"
-    if traffic_file.exists():
+    if traffic_file.exists() and P == 1:
         tf = json.loads(traffic_file.read_text())
         roof["traffic"] = tf.get(f"{args.config}/n{P}/{dom}")
+    nvlink = None
+    if links is not None and (links >= 0).all():
+        # measured link bytes per step and GPU against the algorithmic bytes
+        # (push: source TX / owner RX; pull: owner TX / puller RX)
+        disp_tx, disp_rx = links[:, 2], links[:, 3]
+        comb_tx, comb_rx = links[:, 0] - disp_tx, links[:, 1] - disp_rx
+        per = []
+        for g in range(P):
+            per.append({"gpu": g, "dispatch_tx": disp_tx[g], "dispatch_rx": disp_rx[g],
+                        "alg_dispatch_tx": float(tr["d_eg"][g]), "alg_dispatch_rx": float(tr["d_in"][g]),
+                        "combine_tx": comb_tx[g], "combine_rx": comb_rx[g],
+                        "alg_combine_tx": float(tr["c_eg"][g]), "alg_combine_rx": float(tr["c_in"][g])})
+        meas = {"fs_dispatch": float(np.maximum(disp_tx, disp_rx).max()),
+                "fs_combine": float(np.maximum(comb_tx, comb_rx).max())}
+        nvlink = {
+            "source": f"NVML NVLINK_THROUGHPUT_DATA_TX/RX ({nvc.mode if nvc else 'n/a'}), per step, "
+                      "dispatch from a layout+dispatch-only pass of the same K steps, combine = step - dispatch",
+            "per_gpu_bytes_per_step": [{k: (round(float(v)) if k != "gpu" else v) for k, v in d.items()} for d in per],
+            "bottleneck_bytes": {"fs_dispatch": {"measured": meas["fs_dispatch"], "algorithmic": d_bn},
+                                 "fs_combine": {"measured": meas["fs_combine"], "algorithmic": c_bn}},
+            "measured_over_algorithmic": {k: meas[k] / ((d_bn if k == "fs_dispatch" else c_bn) or 1.0)
+                                          for k in meas},
+            "gbps_per_gpu_measured": {"fs_dispatch": meas["fs_dispatch"] / (k_disp * 1e-3) / 1e9,
+                                      "fs_combine": meas["fs_combine"] / (k_comb * 1e-3) / 1e9},
+        }
+        roof["traffic"] = meas[dom]
+        roof["traffic_src"] = "NVLink data bytes of the bottleneck GPU per launch (NVML counters)"
+    elif P > 1:
+        nvlink = {"unavailable": nvc_err or "counters not readable on every rank"}
 
     line = {
         "metric": METRIC,
@@ -550,20 +637,7 @@ def main() -> int:
         "vs_baseline": None,
         "dtype": dtype,
         "data": "synthetic: reference gen_realworld routing (seed 0) + random payload rows",
-        "config": {
-            "workload": desc,
-            "ep": P,
-            "tokens_per_rank": T_l,
-            "hidden": hidden,
-            "experts": E,
-            "topk": K,
-            "zipf_s": zipf,
-            "expert": "identity (combine pulls the dispatched rows)",
-            "combine_accumulate": "fp32",
-            "l2": f"inputs larger than L2: {NSET} rotating input/output sets + the activation buffer, "
-                  f"{(T_l * tb * 2 + int(tr['rows'].max()) * tb) / 2**20:.0f} MiB touched per step per rank",
-            "value_def": "routed-row bytes (dispatch + combine, all ranks) / step time",
-        },
+        "config": config_dict(args.config, P, int(tr["rows"].max()), NSET),
         "latency_us": ms * 1e3,
         "kernel_us": {"fs_layout": k_layout * 1e3, "fs_dispatch": k_disp * 1e3, "fs_combine": k_comb * 1e3},
         "t_min_us": {"fs_dispatch": t_min_d * 1e6, "fs_combine": t_min_c * 1e6},
@@ -572,7 +646,9 @@ def main() -> int:
             "dispatch": float(tr["d_eg"].mean()) / (k_disp * 1e-3) / 1e9,
             "combine": float(tr["c_eg"].mean()) / (k_comb * 1e-3) / 1e9,
         },
+        "gbps_per_gpu": value / P,
         "roofline": roof,
+        "nvlink_counters": nvlink,
         "gpu_launches": launches,
         "launch_mode": "cuda_graph" if graph is not None else "eager",
         "dispatch_engine": args.dispatch if args.dispatch != "auto" else ("tma" if P == 1 else "warp"),
@@ -585,8 +661,8 @@ def main() -> int:
                        "ms_per_step": e2e_ms / args.steps, "h2d_bytes_per_step": e2e["h2d"] * P,
                        "d2h_bytes_per_step": e2e["d2h"] * P,
                        "pipeline": "3 streams: H2D(j+1) | shuffle(j) | D2H(j-1), pinned host buffers"}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_reference(args.config, 1, args.seed, steps=3, warmup=1, budget_s=25.0)
+    if rank == 0 and not args.no_cpu_baseline:
+        cb = cpu_reference(args.config, world, args.seed, steps=3, warmup=1, budget_s=25.0)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     buf.close()
     if world > 1:

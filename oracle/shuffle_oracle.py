@@ -169,20 +169,30 @@ def combine(act_out: dict, row_of: np.ndarray, experts: np.ndarray, weights: np.
     token_bytes = next(iter(act_out.values())).shape[-1]
     if n == 0:
         return np.zeros((0, token_bytes), dtype=np.uint8)
-    acc = None
-    for k in range(experts.shape[1]):
+
+    def rows_of(k):
         g = owner[experts[token_ids, k]]
         r = row_of[token_ids, k]
-        rows = None
+        rows = np.empty((n, token_bytes), dtype=np.uint8)
         for gg in np.unique(g):
             sel = np.flatnonzero(g == gg)
-            v = decode(act_out[int(gg)][r[sel]], dtype).astype(np.float64)
-            if rows is None:
-                rows = np.empty((n, v.shape[1]), dtype=np.float64)
-            rows[sel] = v
+            rows[sel] = act_out[int(gg)][r[sel]]
+        return rows
+
+    return reduce_rows(rows_of, weights[token_ids], dtype)
+
+
+def reduce_rows(rows_of, weights: np.ndarray, dtype: str = "f32") -> np.ndarray:
+    """engine.py:313-331 _reduce_one: out = Σ_k f64(w[:,k])·f64(row_k), k
+    ascending, one final rounding to the payload dtype.  ``rows_of(k)`` gives
+    the [n, token_bytes] staged rows of column k (what the combine plan
+    delivers to the staging buffer)."""
+    acc = None
+    for k in range(weights.shape[1]):
+        rows = decode(rows_of(k), dtype).astype(np.float64)
         if acc is None:
             acc = np.zeros_like(rows)
-        acc += weights[token_ids, k][:, None] * rows
+        acc += weights[:, k][:, None] * rows
     if dtype == "f32":
         return acc.astype(np.float32).view(np.uint8)
     return np.ascontiguousarray(f64_to_bf16(acc)).view(np.uint8)

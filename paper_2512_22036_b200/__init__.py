@@ -9,6 +9,9 @@ CUDA behind the C ABI in ``include/fusco.h`` (``lib/libfusco.so``).
 
 Public API (reference names kept, see ``api``):
   run_exchange, build_plan_pair, build_plan, dispatch_loads, dedup_ratio,
+  build_dispatch_plan / build_combine_plan / build_direct_plans,
+  allocate_buffers, fill_token_buffers, apply_node_level, apply_expert_level,
+  run_experts, reduce_outputs, execute_dispatch / execute_combine (SPEC.md),
   RoutingAssignment, gen_realworld / gen_single_node / gen_imbalanced,
   ClusterTopology, ExpertPlacement, round_robin_placement, greedy_groups ...
 Per-rank multi-GPU API: ``EPBuffer`` (build_plan / dispatch / combine).
@@ -44,6 +47,17 @@ _LAZY = {
     "run_baseline": "api",
     "build_plan_pair": "api",
     "build_plan": "api",
+    "build_dispatch_plan": "api",
+    "build_combine_plan": "api",
+    "build_direct_plans": "api",
+    "allocate_buffers": "api",
+    "fill_token_buffers": "api",
+    "apply_node_level": "api",
+    "apply_expert_level": "api",
+    "run_experts": "api",
+    "reduce_outputs": "api",
+    "execute_dispatch": "api",
+    "execute_combine": "api",
     "dispatch_loads": "api",
     "dedup_ratio": "api",
     "naive_inter_node_bytes": "api",

@@ -90,6 +90,10 @@ class GpuPlan:
     intra_gpu_bytes: int
     buffer_bytes: dict[str, int]
     loads: np.ndarray            # per-rank dedup send bytes (dispatch_loads)
+    dtype: str = "f32"           # payload element type of the rows ("f32" as in the reference, or "bf16")
+    # the resident device state the executors run on (shared by the dispatch
+    # and combine plans of one routing); None for a host-only plan
+    execution: object = field(default=None, repr=False, compare=False)
 
 
 @dataclass
@@ -181,7 +185,9 @@ def _validate(assignment, topo, placement, token_bytes, mode="analytic", ablate=
 class _Session:
     """Routing of a global assignment split into per-rank device tensors."""
 
-    def __init__(self, assignment, topo, placement, token_bytes, *, with_act_out, device=None, nodedup=False):
+    def __init__(self, assignment, topo, placement, token_bytes, *, with_act_out, device=None, nodedup=False,
+                 dtype="f32"):
+        self.dtype = dtype
         self.P = topo.num_gpus
         self.a = assignment
         self.topo = topo
@@ -247,7 +253,7 @@ class _Session:
             layouts=layouts, local_tokens={s: self.ids[s] for s in range(P)}, row_of=row_of,
             first_mask=first, reduce_weights=reduce_w, inter_bytes_total=inter,
             intra_bytes_total=naive_rows * tb, intra_gpu_bytes=same_gpu, buffer_bytes=buffer_bytes,
-            loads=loads,
+            loads=loads, dtype=self.dtype,
         )
 
 
@@ -265,20 +271,51 @@ def build_plan_pair(
     token_bytes: int,
     balancer: str = "greedy",
     device=None,
+    dtype: str = "f32",
 ) -> tuple[GpuPlan, GpuPlan, np.ndarray]:
-    """Device-planned (dispatch, combine, groups) (reference planner.py:485-497)."""
+    """Device-planned (dispatch, combine, groups) (reference planner.py:485-497):
+    loads, then groups, then both directions.  The plans stay executable
+    (``allocate_buffers`` / ``apply_*`` / ``execute_*`` below) for as long as
+    they are alive."""
     _validate(assignment, topo, placement, token_bytes)
-    sess = _Session(assignment, topo, placement, token_bytes, with_act_out=False, device=device)
-    try:
-        plans = sess.plans()
-        sess.cluster.check()
-        d = sess.host_plan(plans, "dispatch", None)
-        groups = _balancer.build_groups(balancer, d.loads, topo)
-        d.groups = groups
-        c = sess.host_plan(plans, "combine", groups)
-        return d, c, groups
-    finally:
-        sess.close()
+    ex = _execution(assignment, topo, placement, token_bytes, nodedup=False, device=device, dtype=dtype)
+    d = ex.host_plan("dispatch", None)
+    groups = _balancer.build_groups(balancer, d.loads, topo)
+    d.groups = groups
+    c = ex.host_plan("combine", groups)
+    return d, c, groups
+
+
+def build_dispatch_plan(assignment, topo, placement, token_bytes, groups, device=None, dtype: str = "f32") -> GpuPlan:
+    """Deduplicated dispatch plan for a fixed group assignment (reference
+    planner.py:211-339): the device layout planner's row order, per-rank
+    dedup counters and first mask; executable by ``apply_node_level`` /
+    ``apply_expert_level`` / ``execute_dispatch``."""
+    _validate(assignment, topo, placement, token_bytes)
+    _balancer.validate_groups(groups, topo)
+    ex = _execution(assignment, topo, placement, token_bytes, nodedup=False, device=device, dtype=dtype)
+    return ex.host_plan("dispatch", np.asarray(groups))
+
+
+def build_combine_plan(assignment, topo, placement, token_bytes, groups, device=None, dtype: str = "f32") -> GpuPlan:
+    """Return-path plan, no dedup (reference planner.py:342-482): the same
+    device layout, read back by the pull combine; ``reduce_weights`` per
+    source rank.  Executable by ``reduce_outputs`` / ``execute_combine``."""
+    _validate(assignment, topo, placement, token_bytes)
+    _balancer.validate_groups(groups, topo)
+    ex = _execution(assignment, topo, placement, token_bytes, nodedup=False, device=device, dtype=dtype)
+    return ex.host_plan("combine", np.asarray(groups))
+
+
+def build_direct_plans(assignment, topo, placement, token_bytes, device=None, dtype: str = "f32"):
+    """The planner ablation's plans (reference planner.py:563-659): same
+    layouts, no dedup — every remote (token, expert) row crosses the link
+    (the device push with ``fs_set_nodedup``)."""
+    _validate(assignment, topo, placement, token_bytes)
+    ex = _execution(assignment, topo, placement, token_bytes, nodedup=True, device=device, dtype=dtype)
+    d = ex.host_plan("dispatch", None)
+    d.inter_bytes_total = naive_inter_node_bytes(assignment, placement, topo, token_bytes)
+    return d, ex.host_plan("combine", None)
 
 
 # SPEC.md:260 name
@@ -452,3 +489,306 @@ def run_baseline(assignment, topo, placement, token_bytes, *, payload_seed: int 
     return run_exchange(assignment, topo, placement, token_bytes, payload_seed=payload_seed, mode=mode, cost=cost,
                         ablate=("dcomm", "planner"), expert_fn=expert_fn, materialize=materialize, dtype=dtype,
                         acc=acc, device=device)
+
+
+# ---------------------------------------------------------------------------
+# The reference's executor API (engine.py:249-338) over the
+# resident device state of a plan pair.
+#
+# Buffers are a dict ``"kind/rank" -> flat uint8 device tensor`` as in the
+# reference (``planner.py:35-49``).  ``allocate_buffers`` returns
+# ``token/s`` and ``output/s`` (plain device tensors) and ``activation/g`` /
+# ``act_out/g`` — views of rank g's symmetric region, because the dispatch
+# writes every owner's expert-major rows in place over NVLink.  The
+# reference's landing and staging kinds (``fwd_recv``, ``comb_recv``,
+# ``staging``) do not exist here: no byte is staged between the token rows
+# and the expert-major rows, nor between the expert outputs and the
+# reduction.  Stage mapping (each a launch of the fused kernels' phase):
+#
+#   dispatch  apply_node_level    push of every (token, destination rank) row
+#                                 to its owner (one crossing per rank)
+#             apply_expert_level  receiver fan-out of a token's further rows
+#                                 on the same rank
+#   combine   apply_expert_level  owners publish "expert outputs ready"
+#             apply_node_level    (nothing left to move: the pull is fused
+#                                 into the reduction)
+#             reduce_outputs      pull of the K rows + k-ascending weighted sum
+# ---------------------------------------------------------------------------
+
+import hashlib as _hashlib
+import weakref as _weakref
+
+from ._lib import FS_PHASE_LOCAL, FS_PHASE_REMOTE, FS_ACC_F64
+
+_EXECUTIONS: "_weakref.WeakValueDictionary" = _weakref.WeakValueDictionary()
+
+
+def _fingerprint(assignment, placement) -> str:
+    h = _hashlib.sha1()
+    for arr in (assignment.experts, assignment.source, placement.owner):
+        h.update(np.ascontiguousarray(arr, dtype=np.int64).tobytes())
+        h.update(b"|")
+    return h.hexdigest()
+
+
+class _Execution:
+    """A planned shuffle resident on the device: the emulated cluster, its
+    per-rank device plans, and which stages of the current epoch have run."""
+
+    def __init__(self, assignment, topo, placement, token_bytes, *, nodedup, device, dtype):
+        self.sess = _Session(assignment, topo, placement, token_bytes, with_act_out=True, device=device,
+                             nodedup=nodedup, dtype=dtype)
+        self.plans = self.sess.plans()
+        self.sess.cluster.check()
+        self.tdt, self.code = dtype_code(dtype)
+        self.stage: set[str] = set()
+
+    def host_plan(self, direction, groups) -> GpuPlan:
+        p = self.sess.host_plan(self.plans, direction, groups)
+        p.execution = self
+        return p
+
+    def replan(self) -> None:
+        """A new epoch of the same routing (the device plan is recomputed)."""
+        self.sess.cluster.layout_into(self.plans)
+        self.sess.cluster.check()
+        self.stage.clear()
+
+    @property
+    def ranks(self):
+        return self.sess.cluster.ranks
+
+    def rows(self, g: int) -> int:
+        return self.plans[g].num_rows
+
+    def close(self) -> None:
+        self.sess.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _execution(assignment, topo, placement, token_bytes, *, nodedup, device, dtype) -> _Execution:
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    key = (_fingerprint(assignment, placement), topo.num_nodes, topo.gpus_per_node, int(token_bytes),
+           bool(nodedup), str(dev), dtype)
+    ex = _EXECUTIONS.get(key)
+    if ex is None:
+        ex = _Execution(assignment, topo, placement, token_bytes, nodedup=nodedup, device=dev, dtype=dtype)
+        _EXECUTIONS[key] = ex
+    return ex
+
+
+def _exec_of(plan) -> _Execution:
+    ex = getattr(plan, "execution", None)
+    if ex is None:
+        raise ValueError("plan has no device state: build it with build_plan_pair / build_dispatch_plan / "
+                         "build_combine_plan")
+    return ex
+
+
+def allocate_buffers(*plans: GpuPlan) -> dict[str, torch.Tensor]:
+    """Buffers for a plan pair (reference engine.py:249-254), sized by the
+    plans: ``token/s``, ``output/s`` zero-filled device tensors,
+    ``activation/g`` / ``act_out/g`` views of rank g's symmetric rows."""
+    if not plans:
+        raise ValueError("allocate_buffers needs at least one plan")
+    ex = _exec_of(plans[0])
+    if any(_exec_of(p) is not ex for p in plans):
+        raise ValueError("plans of different routings cannot share buffers")
+    tb, dev = plans[0].token_bytes, ex.sess.dev
+    bufs: dict[str, torch.Tensor] = {}
+    for s, ids in enumerate(ex.sess.ids):
+        bufs[f"token/{s}"] = torch.zeros(ids.size * tb, dtype=torch.uint8, device=dev)
+        bufs[f"output/{s}"] = torch.zeros(ids.size * tb, dtype=torch.uint8, device=dev)
+    for g, r in enumerate(ex.ranks):
+        n = ex.rows(g)
+        bufs[f"activation/{g}"] = r.act(n).reshape(-1)
+        bufs[f"act_out/{g}"] = r.act_out(n).reshape(-1)
+    return bufs
+
+
+def _buf(buffers, kind: str, g: int, nbytes: int, region: torch.Tensor | None = None) -> torch.Tensor:
+    name = f"{kind}/{g}"
+    if name not in buffers:
+        raise ValueError(f"missing buffer {name}")
+    b = buffers[name]
+    if not isinstance(b, torch.Tensor) or not b.is_cuda or b.dtype != torch.uint8 or not b.is_contiguous():
+        raise ValueError(f"buffer {name} must be a contiguous uint8 CUDA tensor (allocate_buffers)")
+    if b.numel() != nbytes:
+        raise ValueError(f"buffer {name} holds {b.numel()} bytes, the plan needs {nbytes}")
+    if region is not None and b.data_ptr() != region.data_ptr():
+        raise ValueError(f"buffer {name} must be the symmetric-region view from allocate_buffers "
+                         "(peers write these rows in place)")
+    return b
+
+
+def fill_token_buffers(plan: GpuPlan, buffers, payloads) -> None:
+    """token/s = payload rows of source s's tokens, ascending global id
+    (reference engine.py:257-263)."""
+    ex, tb = _exec_of(plan), plan.token_bytes
+    pay = torch.as_tensor(np.ascontiguousarray(payloads).reshape(plan.num_tokens, tb)) \
+        if not isinstance(payloads, torch.Tensor) else payloads.reshape(plan.num_tokens, tb)
+    for s, ids in enumerate(ex.sess.ids):
+        if ids.size:
+            dst = _buf(buffers, "token", s, ids.size * tb).view(ids.size, tb)
+            dst.copy_(pay[torch.as_tensor(ids, device=pay.device)])
+
+
+def _tokens(ex, buffers, tb):
+    return [_buf(buffers, "token", s, ids.size * tb).view(ids.size, tb) for s, ids in enumerate(ex.sess.ids)]
+
+
+def _check_region_bufs(ex, buffers, kind, tb):
+    for g, r in enumerate(ex.ranks):
+        n = ex.rows(g)
+        _buf(buffers, kind, g, n * tb, r.act(n) if kind == "activation" else r.act_out(n))
+
+
+def apply_node_level(plan: GpuPlan, buffers) -> None:
+    """Dispatch: push every (token, destination rank) row into its owner's
+    expert-major rows (reference engine.py:266-269).  Combine: no separate
+    movement (the pull is fused into ``reduce_outputs``)."""
+    ex, tb = _exec_of(plan), plan.token_bytes
+    if plan.direction == "dispatch":
+        xs = _tokens(ex, buffers, tb)
+        _check_region_bufs(ex, buffers, "activation", tb)
+        if "d_node" in ex.stage:  # a repeated dispatch of the same routing: a new epoch
+            ex.replan()
+        for r, x, p in zip(ex.ranks, xs, ex.plans):
+            r.dispatch(x, p, FS_PHASE_LOCAL)
+        ex.stage.add("d_node")
+        return
+    if "c_expert" not in ex.stage:
+        raise ValueError("combine: apply_expert_level first (expert outputs leave their owners first)")
+    ex.stage.add("c_node")
+
+
+def apply_expert_level(plan: GpuPlan, buffers) -> None:
+    """Dispatch: receiver fan-out of each token's further rows on the same
+    rank (reference engine.py:272-276).  Combine: owners publish their
+    expert outputs to the pulling ranks."""
+    ex, tb = _exec_of(plan), plan.token_bytes
+    if plan.direction == "dispatch":
+        if "d_node" not in ex.stage or "d_expert" in ex.stage:
+            raise ValueError("dispatch: apply_node_level first (once per expert-level pass)")
+        xs = _tokens(ex, buffers, tb)
+        for r, x, p in zip(ex.ranks, xs, ex.plans):
+            r.dispatch(x, p, FS_PHASE_REMOTE)
+        ex.sess.cluster.check()
+        ex.stage.add("d_expert")
+        return
+    if "d_expert" not in ex.stage:
+        raise ValueError("combine before dispatch")
+    _combine_phase(ex, plan, buffers, FS_PHASE_LOCAL, None)
+    ex.stage.add("c_expert")
+
+
+def run_experts(plan: GpuPlan, buffers, expert_fn) -> None:
+    """activation -> act_out on every rank through the row-aligned expert map
+    (reference engine.py:295-310).  ``expert_fn(act_f32 [rows, width] CUDA
+    tensor, expert_ids [rows] CUDA int64) -> [rows, width]``."""
+    ex, tb = _exec_of(plan), plan.token_bytes
+    if "d_expert" not in ex.stage:
+        raise ValueError("run_experts before the dispatch completed")
+    _check_region_bufs(ex, buffers, "activation", tb)
+    _check_region_bufs(ex, buffers, "act_out", tb)
+    dev = ex.sess.dev
+    for g, (r, p) in enumerate(zip(ex.ranks, ex.plans)):
+        n = ex.rows(g)
+        if n == 0:
+            continue
+        eids = torch.repeat_interleave(torch.as_tensor(r.local_experts, device=dev), p.expert_counts.to(torch.int64))
+        act = r.act(n, ex.tdt)
+        y = expert_fn(act.to(torch.float32), eids)
+        if not isinstance(y, torch.Tensor) or tuple(y.shape) != tuple(act.shape):
+            raise ValueError("expert function must return a tensor of the activation shape")
+        r.act_out(n, ex.tdt).copy_(y.to(ex.tdt))
+    ex.stage.add("experts")
+
+
+def _weights_for(ex, plan, s, weights):
+    if weights is None:
+        w = plan.reduce_weights[s]
+    elif isinstance(weights, dict):
+        w = weights[s]
+    else:
+        w = np.asarray(weights)[ex.sess.ids[s]]
+    return torch.as_tensor(np.ascontiguousarray(w, dtype=np.float64), device=ex.sess.dev)
+
+
+def _combine_phase(ex, plan, buffers, phase, weights):
+    tb = plan.token_bytes
+    width = tb // torch.empty(0, dtype=ex.tdt).element_size()
+    src = FS_SRC_ACT_OUT if "experts" in ex.stage else FS_SRC_ACT
+    for s, (r, p) in enumerate(zip(ex.ranks, ex.plans)):
+        n = ex.sess.ids[s].size
+        out = _buf(buffers, "output", s, n * tb).view(ex.tdt).view(n, width)
+        r.combine(p, _weights_for(ex, plan, s, weights), out, dtype_code=ex.code, src=src, acc=FS_ACC_F64,
+                  phase=phase)
+
+
+def reduce_outputs(plan: GpuPlan, buffers, weights=None) -> None:
+    """output/s[t] = Σ_k w[t,k]·(expert output of (t,k)), f64, k ascending,
+    one rounding (reference engine.py:313-338), pulled straight from the
+    owners' rows.  ``weights`` overrides ``plan.reduce_weights`` ([T, K]
+    global or a per-source dict)."""
+    if plan.reduce_weights is None:
+        raise ValueError("not a combine plan")
+    ex = _exec_of(plan)
+    if "d_expert" not in ex.stage:
+        raise ValueError("combine before dispatch")
+    if "c_expert" not in ex.stage:
+        apply_expert_level(plan, buffers)
+    _combine_phase(ex, plan, buffers, FS_PHASE_REMOTE, weights)
+    ex.sess.cluster.check()
+    ex.stage.add("reduced")
+
+
+def _timed(fn):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    fn()
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) * 1e-3
+
+
+def execute_dispatch(plan: GpuPlan, buffers, mode: str = "analytic"):
+    """run the dispatch plan: returns ({g: activation rows}, PhaseReport)."""
+    if plan.direction != "dispatch":
+        raise ValueError("not a dispatch plan")
+    if mode not in ("analytic", "wallclock"):
+        raise ValueError(f"unknown mode {mode!r}")
+
+    def run():
+        apply_node_level(plan, buffers)
+        apply_expert_level(plan, buffers)
+
+    t = _timed(run)
+    acts = {g: buffers[f"activation/{g}"] for g in range(len(_exec_of(plan).ranks))}
+    rep = PhaseReport("dispatch", mode, 0.0, 0.0, t, plan.inter_bytes_total, plan.intra_bytes_total,
+                      plan.intra_gpu_bytes, 0)
+    return acts, rep
+
+
+def execute_combine(combine_plan: GpuPlan, activation_out_buffers, weights=None, mode: str = "analytic"):
+    """run the combine plan over the expert outputs: returns
+    ({s: output rows}, PhaseReport).  The reduction uses ``weights`` ([T, K]
+    or per-source) when given, else the plan's ``reduce_weights``."""
+    if combine_plan.direction != "combine":
+        raise ValueError("not a combine plan")
+
+    def run():
+        apply_expert_level(combine_plan, activation_out_buffers)
+        apply_node_level(combine_plan, activation_out_buffers)
+        reduce_outputs(combine_plan, activation_out_buffers, weights)
+
+    t = _timed(run)
+    outs = {s: activation_out_buffers[f"output/{s}"] for s in range(len(_exec_of(combine_plan).ranks))}
+    rep = PhaseReport("combine", mode, 0.0, 0.0, t, combine_plan.inter_bytes_total, combine_plan.intra_bytes_total,
+                      combine_plan.intra_gpu_bytes, 0)
+    return outs, rep

@@ -18,9 +18,9 @@ namespace cg = cooperative_groups;
 // each destination row, the row holding its bytes (fan_src): itself, or the
 // primary row of the same token on that rank.  After every source's CTAs
 // have signalled arrival, the receiver copies primary -> duplicate rows in
-// its own HBM.  The activation buffer is double-buffered by epoch parity so
-// that a fast rank's next dispatch cannot overwrite rows a slow rank is
-// still pulling in combine.
+// its own HBM.  The activation buffer is single: a rank's next dispatch
+// cannot start before every peer published its next-epoch counts, i.e.
+// finished pulling this epoch's rows in combine (fusco.cu region_layout).
 // ===========================================================================
 template <typename V>
 struct MoveCfg {
@@ -85,7 +85,10 @@ __device__ __forceinline__ void fan_out_rows(const FsArgs& a, size_t act_off, si
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
-  const int rows = *reinterpret_cast<volatile int*>(a.num_rows);
+  // the planner records FS_ERANGE (and fs_check raises) when the rows exceed
+  // the buffer; never walk past it meanwhile
+  const long long rows_all = *reinterpret_cast<volatile int*>(a.num_rows);
+  const int rows = (int)(rows_all < a.max_rows ? rows_all : a.max_rows);
   const int S = (nv + SW - 1) / SW;
   const int32_t* fs = reinterpret_cast<const int32_t*>(a.peer[a.rank] + fan_off);
   V* act = reinterpret_cast<V*>(a.peer[a.rank] + act_off);

@@ -77,6 +77,8 @@ struct fs_ctx {
   int combine_grid_cap; // 0 = occupancy-derived
   size_t layout_smem;
   uint32_t epoch;
+  int disp_phases;  // dispatch phases already enqueued in this epoch (each runs once)
+  int comb_phases;  // combine phases already enqueued in this epoch (repeats reset the claim counter)
   unsigned long long timeout_ns;
   RegionLayout L;
   std::vector<char*> peers;
@@ -507,7 +509,10 @@ int fs_layout(fs_handle_t h, const void* topk_idx, int idx_bytes, int num_tokens
     return fail(FS_EINVAL, "num_tokens outside [0, max_tokens]");
   if ((phase & FS_PHASE_ALL) == 0 || (phase & ~FS_PHASE_ALL)) return fail(FS_EINVAL, "bad phase");
   if (num_tokens > 0 && (!topk_idx || !row_of)) return fail(FS_EINVAL, "null topk_idx / row_of");
-  if (phase & FS_PHASE_LOCAL) h->epoch++;
+  if (phase & FS_PHASE_LOCAL) {
+    h->epoch++;
+    h->disp_phases = h->comb_phases = 0;
+  }
   FsArgs a = make_args(h, num_tokens, idx_bytes == 8);
   long long* st_ptr = reinterpret_cast<long long*>(stats);
   const int ncl = (num_tokens + kClusterThreads - 1) / kClusterThreads;
@@ -548,6 +553,10 @@ int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_byte
   if ((phase & FS_PHASE_ALL) == 0 || (phase & ~FS_PHASE_ALL)) return fail(FS_EINVAL, "bad phase");
   if (num_tokens > 0 && (!x || !topk_idx || !row_of)) return fail(FS_EINVAL, "null input");
   if (h->epoch == 0) return fail(FS_EINVAL, "fs_dispatch before fs_layout");
+  // the push claims / done counts / arrival flags are per epoch: a second
+  // dispatch of the same phase needs a new plan (fs_layout) first
+  if (h->disp_phases & phase) return fail(FS_EINVAL, "fs_dispatch already ran for this plan: call fs_layout first");
+  h->disp_phases |= phase;
   FsArgs a = make_args(h, num_tokens, idx_bytes == 8);
   const bool vec16 = (h->tb % 16 == 0) && aligned(x, 16);
   if (!aligned(x, 4)) return fail(FS_EINVAL, "x must be 4-byte aligned");
@@ -606,6 +615,14 @@ int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes, const int32_t
   if (acc != FS_ACC_F32 && acc != FS_ACC_F64) return fail(FS_EINVAL, "acc must be f32 or f64");
   if (num_tokens > 0 && (!topk_idx || !row_of || !topk_w || !out)) return fail(FS_EINVAL, "null input");
   if (h->epoch == 0) return fail(FS_EINVAL, "fs_combine before fs_layout");
+  if (h->comb_phases & phase & FS_PHASE_REMOTE) {
+    // a repeated combine of the same plan (e.g. another expert output):
+    // re-arm the dynamic item counter (both parities: the other one is the
+    // next epoch's, zeroed by its planner anyway), stream-ordered and graph-safe
+    for (int q = 0; q < 2; ++q)
+      FS_CUDA(cudaMemsetAsync(h->work_d + q * 8 + kWorkCombine, 0, sizeof(unsigned long long), (cudaStream_t)stream));
+  }
+  h->comb_phases |= phase;
   FsArgs a = make_args(h, num_tokens, idx_bytes == 8);
   if (!aligned(out, 4)) return fail(FS_EINVAL, "out must be 4-byte aligned");
   const bool vec16 = (h->tb % 16 == 0) && aligned(out, 16);

@@ -2,9 +2,10 @@
 //
 // Memory-ordering protocol over NVLink/NVSwitch (replaces the reference's
 // ring-buffer + expected-byte counters, engine.py:637-694, 979-1031):
-//   writer: payload stores (weak st.global to peer addresses)
-//           -> fence.sc.sys by every writing thread -> bar.sync
-//           -> one thread: st.release.sys / red.release.sys on the peer flag
+//   writer: payload stores (weak st.global to peer addresses) -> bar.sync
+//           -> thread 0: fence.acq_rel.sys, then an acq_rel.gpu count on a
+//              local counter; the last arrival issues st.release.sys on the
+//              peer flag (signal_pushed below)
 //   reader: one thread per flag spins ld.acquire.sys until the epoch value
 //           -> bar.sync -> payload loads.
 // Flags never reset: they carry the monotonically increasing epoch (or an
@@ -185,13 +186,15 @@ __device__ __forceinline__ void gather_counts(const FsArgs& a, int parity, uint3
   *before = b;
 }
 
-// End of a rank's push phase: every CTA counts itself done on a local
-// counter (acq_rel, cumulative over the CTA's stores through bar.sync); the
-// last CTA of the epoch then releases one flag per peer (value = epoch).
-// One NVLink signal per (source, destination) instead of one per CTA.
+// End of a rank's push phase: every CTA makes its peer stores visible at
+// system scope (bar.sync, then one fence.acq_rel.sys by thread 0) and counts
+// itself done on a local counter; the last CTA of the epoch then releases
+// one flag per peer (value = epoch).  One NVLink signal per (source,
+// destination) instead of one per CTA.
 __device__ __forceinline__ void signal_pushed(const FsArgs& a, uint32_t epoch) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence_system();
     // per-parity counter, zeroed by the planner for the next epoch, so the
     // grid may differ between launches
     unsigned long long* done = a.work + (size_t)(epoch & 1u) * 8 + kWorkDone;

@@ -575,7 +575,13 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
       stats[slot[tid]] = acc;
     }
     if (stats && tid >= 5 && tid < FS_NSTATS) stats[tid] = 0;
-    if (tid < 8) a.work[(size_t)(parity ^ 1) * 8 + tid] = 0ull;
+    // the next epoch's accumulators (the grid planner relies on them being
+    // zeroed one epoch ahead, and either planner may run next)
+    for (int e = tid; e < E; e += kClusterThreads) a.totals[(size_t)(parity ^ 1) * E + e] = 0;
+    if (tid < 8) {
+      a.stat_part[(parity ^ 1) * 8 + tid] = 0;
+      a.work[(size_t)(parity ^ 1) * 8 + tid] = 0ull;
+    }
     if (tid == 0) *a.epoch_ptr = epoch;  // every CTA read the old epoch before the cluster barrier
     trace_stamp(a, FS_TRACE_LAYOUT_PUBLISH);
   }

@@ -261,6 +261,13 @@ class Rank:
             raise ValueError(f"topk_w must be f32/f64 [T, {self.topk}]")
         if not topk_w.is_contiguous() or not out.is_contiguous():
             raise ValueError("topk_w and out must be contiguous")
+        if topk_w.device != self.device or out.device != self.device:
+            raise ValueError("topk_w and out must be on the rank's device")
+        want_dt = {FS_DTYPE_F32: torch.float32, FS_DTYPE_BF16: torch.bfloat16}.get(dtype_code)
+        if want_dt is None or out.dtype != want_dt:
+            raise ValueError(f"out must be {want_dt} for dtype_code {dtype_code}")
+        if out.numel() * out.element_size() != plan.num_tokens * self.token_bytes:
+            raise ValueError("out must hold num_tokens x token_bytes bytes")
         if plan.epoch != self.epoch:
             raise ValueError("plan is stale: combine must follow its own dispatch")
         call(

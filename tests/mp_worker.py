@@ -24,7 +24,10 @@ def main() -> int:
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     P, rank = dist.get_world_size(), dist.get_rank()
-    E, K, T_l = int(os.environ.get("MP_E", 64)), int(os.environ.get("MP_K", 8)), 256
+    E, K = int(os.environ.get("MP_E", 64)), int(os.environ.get("MP_K", 8))
+    T_l = int(os.environ.get("MP_T", 256))  # tokens per rank (BASELINE sizes: 4096 / 8192)
+    iters = int(os.environ.get("MP_ITERS", 4))
+    big = T_l > 1024  # full-size check: activations on the device, combine on sampled tokens
     H = int(os.environ.get("MP_H", 2048))
     dt = os.environ.get("MP_DT", "bf16")
     topo = box(P)
@@ -34,7 +37,7 @@ def main() -> int:
     base = DisaggregatedShuffle(num_experts=E, topk=K)
     dev = torch.device("cuda", local)
     failures = 0
-    for it in range(4):
+    for it in range(iters):
         a = gen_realworld(P * T_l, K, topo, pl, seed=10 + it, zipf_s=0.4 * it)
         vals = np.random.default_rng(it).standard_normal((a.num_tokens, H)).astype(np.float32)
         payload = O.encode(vals, dt)
@@ -52,13 +55,30 @@ def main() -> int:
             out = buf.combine(plan, w, src="act", acc="f64")
         buf.check()
         layouts, row_of = O.activation_layouts(a.experts, a.source, pl.owner, P)
+        if not np.array_equal(plan.row_of.cpu().numpy(), row_of[ids]):
+            print(f"[rank {rank}] iter {it}: row_of mismatch", flush=True)
+            failures += 1
+        if big:
+            # oracle dispatch evaluated on the device: row r holds token_ids[r]'s payload
+            pay_d = torch.as_tensor(payload, device=dev)
+            want_act = O.dispatch(pay_d, {rank: layouts[rank]})[rank]
+            if not torch.equal(act[:rows].contiguous().view(torch.uint8).reshape(rows, -1), want_act):
+                print(f"[rank {rank}] iter {it}: activation mismatch", flush=True)
+                failures += 1
+            # identity expert: every staged row of token t is x_t; oracle reduction on 1024 sampled tokens
+            loc = np.sort(np.random.default_rng(it).choice(ids.size, size=min(ids.size, 1024), replace=False))
+            t = ids[loc]
+            want = O.reduce_rows(lambda k: payload[t], a.weights[t], dt)
+            got = out.view(torch.uint8).reshape(ids.size, -1)[torch.as_tensor(loc, device=dev)].cpu().numpy()
+            if not np.array_equal(got, want):
+                print(f"[rank {rank}] iter {it}: output mismatch", flush=True)
+                failures += 1
+            del pay_d
+            continue
         acts = O.dispatch(payload, layouts)
         got_act = act[:rows].contiguous().view(torch.uint8).cpu().numpy().reshape(rows, -1)
         if not np.array_equal(got_act, acts[rank]):
             print(f"[rank {rank}] iter {it}: activation mismatch", flush=True)
-            failures += 1
-        if not np.array_equal(plan.row_of.cpu().numpy(), row_of[ids]):
-            print(f"[rank {rank}] iter {it}: row_of mismatch", flush=True)
             failures += 1
         want = O.combine(acts, row_of, a.experts, a.weights, pl.owner, ids, dt)
         if not np.array_equal(out.view(torch.uint8).cpu().numpy(), want):
