@@ -295,6 +295,11 @@ def run_nccl_baseline(args, world, rank, local, dev) -> int:
 
 def main() -> int:
     args = parse()
+    wd = float(os.environ.get("FUSCO_BENCH_WATCHDOG_S", "0"))
+    if wd > 0:  # diagnostics: dump every thread's stack and exit if the run hangs
+        import faulthandler
+
+        faulthandler.dump_traceback_later(wd, exit=True)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -437,16 +442,14 @@ def main() -> int:
         for _ in range(3):
             graph.replay()
     nvc, nvc_err = None, None
-    if P > 1:  # NVLink data counters around the timed region (ncu cannot wrap a multi-rank run)
+    if P > 1:  # NVLink data counters (ncu cannot wrap a multi-rank run)
         try:
             from paper_2512_22036_b200.nvlink import NvlinkCounters
 
             nvc = NvlinkCounters(dev)
-            nvc.read()
         except Exception as e:  # measurement only: report why it is missing
             nvc, nvc_err = None, repr(e)
     barrier()
-    link0 = nvc.read() if nvc else None
     host0 = time.perf_counter()
     start.record()
     if graph is not None:
@@ -460,23 +463,29 @@ def main() -> int:
     end.record()
     host_ms = (time.perf_counter() - host0) * 1e3
     barrier()
-    link1 = nvc.read() if nvc else None
     buf.check()
     total_ms = start.elapsed_time(end)
-    link_disp = None
-    if nvc:  # the same K steps without the combine: the dispatch's (and planner's) own link bytes
-        for i in range(args.steps):
+    link_step = link_disp = None
+    n_cnt = max(args.steps, 200)  # counter passes: long enough for the NVML sampling
+    if nvc:
+        # whole steps, then the same number without the combine (the
+        # dispatch's and planner's own link bytes); outside the timed region
+        nvc.start()
+        for i in range(n_cnt):
+            step(i)
+        barrier()
+        link_step = nvc.stop()
+        for i in range(n_cnt):
             f_layout(*lay_args)
             f_disp(*disp_args[i % NSET])
         barrier()
-        d0 = nvc.read()
-        for i in range(args.steps):
+        nvc.start()
+        for i in range(n_cnt):
             f_layout(*lay_args)
             f_disp(*disp_args[i % NSET])
         barrier()
-        d1 = nvc.read()
+        link_disp = nvc.stop()
         buf.check()
-        link_disp = (d1[0] - d0[0], d1[1] - d0[1])
     if graph is not None:  # per-kernel split from an eager pass of the same K steps
         barrier()
         for i in range(args.steps):
@@ -556,11 +565,11 @@ def main() -> int:
     links = None
     if world > 1:
         dist.all_reduce(vec, op=dist.ReduceOp.MAX)
-        lk = torch.tensor([float(link1[0] - link0[0]), float(link1[1] - link0[1]), float(link_disp[0]),
-                           float(link_disp[1])] if nvc else [-1.0] * 4, dtype=torch.float64, device=dev)
+        lk = torch.tensor([float(link_step[0]), float(link_step[1]), float(link_disp[0]), float(link_disp[1])]
+                          if nvc else [-1.0] * 4, dtype=torch.float64, device=dev)
         allk = [torch.empty_like(lk) for _ in range(world)]
         dist.all_gather(allk, lk)
-        links = torch.stack(allk).cpu().numpy() / args.steps  # [P, 4] bytes per step
+        links = torch.stack(allk).cpu().numpy() / n_cnt  # [P, 4] bytes per step
     total_ms, k_layout, k_disp, k_comb, e2e_ms = vec.tolist()
     ms = total_ms / args.steps
     routed = 2.0 * P * T_l * K * tb  # bytes per step, whole job
@@ -609,8 +618,9 @@ def main() -> int:
         meas = {"fs_dispatch": float(np.maximum(disp_tx, disp_rx).max()),
                 "fs_combine": float(np.maximum(comb_tx, comb_rx).max())}
         nvlink = {
-            "source": f"NVML NVLINK_THROUGHPUT_DATA_TX/RX ({nvc.mode if nvc else 'n/a'}), per step, "
-                      "dispatch from a layout+dispatch-only pass of the same K steps, combine = step - dispatch",
+            "source": f"NVML NVLink data counters ({nvc.mode if nvc else 'n/a'}) over {n_cnt} steps after the "
+                      "timed region; dispatch from a layout+dispatch-only pass of as many steps, combine = step - "
+                      "dispatch",
             "per_gpu_bytes_per_step": [{k: (round(float(v)) if k != "gpu" else v) for k, v in d.items()} for d in per],
             "bottleneck_bytes": {"fs_dispatch": {"measured": meas["fs_dispatch"], "algorithmic": d_bn},
                                  "fs_combine": {"measured": meas["fs_combine"], "algorithmic": c_bn}},

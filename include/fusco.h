@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define FS_ABI_VERSION 1
+#define FS_ABI_VERSION 2
 #define FS_MAX_RANKS 32
 
 /* return codes */
@@ -103,8 +103,10 @@ const char* fs_last_error(void);
 
 /* ---- symmetric memory: one region per rank, identical layout everywhere -- */
 
-/* Bytes of one rank's symmetric region for this configuration. */
-int fs_region_bytes(int world, int num_experts, int token_bytes,
+/* Bytes of one rank's symmetric region for this configuration (count
+ * words, dispatch block words and duplicate lists, activation rows,
+ * optional expert-output rows). */
+int fs_region_bytes(int world, int num_experts, int topk, int token_bytes, int max_tokens,
                     long long max_rows, int with_act_out, size_t* bytes_out);
 
 /* cudaMalloc + zero-fill on `device` (not the torch caching allocator, so
@@ -149,6 +151,14 @@ unsigned int fs_epoch(fs_handle_t h);
  * build_direct_plans planner.py:563-659).  Takes effect from the next
  * fs_dispatch; set it identically on every rank. */
 int fs_set_nodedup(fs_handle_t h, int on);
+/* Load balancer on (1, default) or off (0) — the reference's "balancer"
+ * ablation (balancer.py:73-90, engine.py:384-420).  On: push units,
+ * fan-out units and combine items are claimed dynamically from per-epoch
+ * counters, and each token's destination order is rotated so concurrent
+ * warps of a rank spread their first stores over different peers.  Off:
+ * static striding of the same work over the grid, no rotation.  Takes
+ * effect from the next kernel; set it identically on every rank. */
+int fs_set_balance(fs_handle_t h, int on);
 
 /* ---- the hot path --------------------------------------------------------- */
 

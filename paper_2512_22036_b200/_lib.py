@@ -17,6 +17,7 @@ from pathlib import Path
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libfusco.so"
 HEADER = Path(__file__).resolve().parent.parent / "include" / "fusco.h"
 
+FS_ABI_VERSION = ABI_VERSION = 2
 FS_OK, FS_EINVAL, FS_ECUDA, FS_ETIMEOUT, FS_ERANGE = 0, -1, -2, -3, -4
 FS_PHASE_LOCAL, FS_PHASE_REMOTE, FS_PHASE_ALL = 1, 2, 3
 FS_DTYPE_F32, FS_DTYPE_BF16 = 0, 1
@@ -30,7 +31,7 @@ STAT_ROWS, STAT_DEDUP_SEND, STAT_NAIVE_SEND, STAT_LOCAL_ROWS, STAT_NODE_DEDUP = 
 SIGNATURES = {
     "fs_abi_version": (c_int, []),
     "fs_last_error": (c_char_p, []),
-    "fs_region_bytes": (c_int, [c_int, c_int, c_int, c_longlong, c_int, POINTER(c_size_t)]),
+    "fs_region_bytes": (c_int, [c_int, c_int, c_int, c_int, c_int, c_longlong, c_int, POINTER(c_size_t)]),
     "fs_sym_alloc": (c_int, [c_int, c_size_t, POINTER(c_void_p)]),
     "fs_sym_free": (c_int, [c_int, c_void_p]),
     "fs_ipc_handle": (c_int, [c_int, c_void_p, c_void_p]),
@@ -48,6 +49,7 @@ SIGNATURES = {
     "fs_max_rows": (c_longlong, [c_void_p]),
     "fs_epoch": (c_uint, [c_void_p]),
     "fs_set_nodedup": (c_int, [c_void_p, c_int]),
+    "fs_set_balance": (c_int, [c_void_p, c_int]),
     "fs_layout": (
         c_int,
         [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
@@ -97,7 +99,7 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.fs_abi_version() != 1:
+    if lib.fs_abi_version() != ABI_VERSION:
         raise FuscoError(FS_ECUDA, "libfusco ABI version mismatch")
     if path is None:
         _lib = lib

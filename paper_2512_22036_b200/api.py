@@ -186,7 +186,7 @@ class _Session:
     """Routing of a global assignment split into per-rank device tensors."""
 
     def __init__(self, assignment, topo, placement, token_bytes, *, with_act_out, device=None, nodedup=False,
-                 dtype="f32"):
+                 dtype="f32", balance=True):
         self.dtype = dtype
         self.P = topo.num_gpus
         self.a = assignment
@@ -199,7 +199,7 @@ class _Session:
         self.cluster = EmulatedCluster(
             self.P, placement.num_experts, assignment.topk, token_bytes, max_t,
             owner=placement.owner, node_of=topo.node_table(), with_act_out=with_act_out, device=self.dev,
-            nodedup=nodedup,
+            nodedup=nodedup, balance=balance,
         )
         self.idx = [torch.as_tensor(assignment.experts[i], dtype=torch.int64, device=self.dev).contiguous()
                     for i in self.ids]
@@ -259,9 +259,10 @@ class _Session:
 
 def _open_session(assignment, topo, placement, token_bytes, ablate, *, with_act_out, device=None) -> _Session:
     """A session whose ranks push without dedup when ``planner`` is ablated
-    (every (token, k) row crosses the link, ``fs_set_nodedup``)."""
+    (every (token, k) row crosses the link, ``fs_set_nodedup``) and stride
+    their work statically when ``balancer`` is ablated (``fs_set_balance``)."""
     return _Session(assignment, topo, placement, token_bytes, with_act_out=with_act_out, device=device,
-                    nodedup="planner" in ablate)
+                    nodedup="planner" in ablate, balance="balancer" not in ablate)
 
 
 def build_plan_pair(
@@ -366,9 +367,11 @@ def run_exchange(
     """Plan, dispatch, run experts, combine — on the GPU (reference engine.py:374-460).
 
     ``mode``/``cost`` are accepted for signature compatibility: both modes
-    execute the real kernels and report CUDA-event times.  The ``planner`` and
-    ``dcomm`` ablations (no dedup / disaggregated pack-a2a-unpack) are the
-    next-row GPU baseline and are not implemented on this path yet.
+    execute the real kernels and report CUDA-event times.  Ablations:
+    ``planner`` pushes every (token, k) row (no dedup), ``balancer`` turns
+    the device balancing off (static work striding, no rotation) and the
+    groups to "static", ``dcomm`` runs the disaggregated pack / all-to-all /
+    unpack baseline.
     """
     ablate = _validate(assignment, topo, placement, token_bytes, mode, ablate)
     tdt, code = dtype_code(dtype)

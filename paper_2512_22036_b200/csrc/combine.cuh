@@ -418,7 +418,9 @@ __global__ void __launch_bounds__(kCombThreads)
       return w64 ? (Acc)reinterpret_cast<const double*>(topk_w)[pos]
                  : (Acc)reinterpret_cast<const float*>(topk_w)[pos];
     };
-    long long u = claim_warp(ctr);
+    // balancer on: items claimed dynamically; off: static striding over the CTAs
+    const bool dyn = a.balance != 0;
+    long long u = dyn ? claim_warp(ctr) : (long long)blockIdx.x;
     KMeta m = u < items ? load_meta(a, idx, row_of, (int)((uint32_t)u / (uint32_t)S), lane) : KMeta{0, 0};
     Acc wl = u < items ? load_w(u) : (Acc)0;
     int n = 0;
@@ -432,7 +434,7 @@ __global__ void __launch_bounds__(kCombThreads)
         }
         break;
       }
-      const long long un = claim_warp(ctr);  // claimed and prefetched while this item streams
+      const long long un = dyn ? claim_warp(ctr) : u + gridDim.x;  // claimed and prefetched while this item streams
       KMeta mn = KMeta{0, 0};
       Acc wn = (Acc)0;
       if (un < items) {

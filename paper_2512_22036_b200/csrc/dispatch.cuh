@@ -70,57 +70,188 @@ __device__ __forceinline__ void warp_copy_row_cg(V* __restrict__ dst, const V* _
   }
 }
 
-// Receiver-side fan-out: rows whose fan_src points at another row (a
-// duplicate destination of a token that crossed NVLink once) are copied from
-// that primary row.  Two steps over the whole (cooperative) grid: every warp
-// scans 32 rows per load (most rows are primaries) and appends the
-// duplicates to a list with one atomic per warp; after a grid barrier the
-// (row, slice) copy units of the list are strided over every warp.  Balanced
-// whatever the duplicates' distribution over the rows (sources, experts).
+// ===========================================================================
+// Receiver-side fan-out, block by block as the pushes land (P > 1)
+//
+// Jobs are (source q, block b).  One watcher warp (CTA 0's last warp) polls
+// the block words of every pending job — lane l owns jobs l, l+32, ... in
+// block-major order — and publishes each landed job with its duplicate
+// count: jcum[k] (cumulative fan-out units after the k-th published job),
+// jorder[k] = (q << 16) | b, then one release of (k << 40 | units) on the
+// work word kWorkFanReady.  Every other warp with nothing left to push
+// claims groups of kFanGroup units (one unit = one kSliceWords slice of one
+// duplicate row) and copies primary -> duplicate rows in its own HBM once
+// the published prefix covers them — so duplicates of early blocks are
+// fanned out while later blocks are still crossing NVLink.  Replaces the
+// reference's "forwarders fan out after all landings" (engine.py:845-847)
+// and its expected-byte completion counters (engine.py:979-1031).
+// ===========================================================================
+constexpr int kFanGroup = 4;
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+constexpr unsigned long long kUnitMask = (1ull << 40) - 1;
+
+// The watcher warp: publishes landed jobs until every one is in (or timeout).
+static __device__ void fan_watch(const FsArgs& a, uint32_t epoch, int S) {
+  const int P = a.world, s = a.rank, lane = threadIdx.x & 31;
+  const int par = (int)(epoch & 1u);
+  unsigned long long* ready = work_ctr(a, epoch, kWorkFanReady);
+  unsigned long long* done = work_ctr(a, epoch, kWorkFanDone);
+  // blocks per source from the sources' published token counts
+  int nb = 0;
+  if (lane < P && lane != s) {
+    const int Tq = read_count_word(a, par, epoch, lane, a.E);
+    nb = (Tq + kBlockTokens - 1) / kBlockTokens;
+  }
+  int nbm = nb;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nbm = max(nbm, __shfl_xor_sync(kFull, nbm, o));
+  const int Q = P - 1;
+  const int J = nbm * Q;
+  int j = lane;  // this lane's next pending job (block-major, sources rotated by the receiver)
+  unsigned long long units = 0;
+  uint32_t npub = 0;
+  const unsigned long long t0 = globaltimer();
+  bool timed_out = false;
+  while (__any_sync(kFull, j < J)) {
+    bool rdy = false;
+    uint32_t nd = 0;
+    int q = 0, b = 0;
+    if (j < J) {
+      b = j / Q;
+      q = (s + 1 + j % Q) % P;
+    }
+    // lane q holds nb for source q: fetch the one this lane's job needs
+    const int nb_q = __shfl_sync(kFull, nb, q & 31);
+    if (j < J) {
+      if (b >= nb_q) {
+        rdy = true;  // the source has fewer blocks: nothing to wait for
+      } else {
+        const unsigned long long w = ld_acquire_sys_u64(blkflag_ptr(a, s, q, b));
+        if ((uint32_t)(w >> 32) == epoch) {
+          rdy = true;
+          nd = (uint32_t)w;
+        }
+      }
+    }
+    const bool pub = rdy && nd > 0;
+    const unsigned long long mine = pub ? (unsigned long long)nd * (unsigned long long)S : 0ull;
+    // inclusive warp scan of the newly published units
+    unsigned long long inc = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long n = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += n;
+    }
+    const uint32_t pm = __ballot_sync(kFull, pub);
+    if (pub) {
+      const uint32_t k = npub + __popc(pm & ((1u << lane) - 1u));
+      a.fan_jcum[k] = units + inc;
+      a.fan_jorder[k] = ((uint32_t)q << 16) | (uint32_t)b;
+    }
+    units += __shfl_sync(kFull, inc, 31);
+    npub += __popc(pm);
+    if (rdy) j += 32;
+    __syncwarp();
+    if (pm && lane == 0) st_release_gpu_u64(ready, ((unsigned long long)npub << 40) | units);
+    if (!pm) {
+      if (globaltimer() - t0 > a.timeout_ns) {
+        timed_out = true;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  if (timed_out && lane == 0) record_error(a.status, FS_ETIMEOUT);
+  if (a.trace != nullptr && lane == 0) a.trace[FS_TRACE_DISPATCH_ARRIVED] = globaltimer();
+  __syncwarp();
+  if (lane == 0) st_release_gpu_u64(done, 1ull);
+}
+
+// A fan-out worker warp: claims unit groups and copies duplicate slices.
 template <typename V>
-__device__ __forceinline__ void fan_out_rows(const FsArgs& a, size_t act_off, size_t fan_off, int nv,
-                                             uint32_t epoch) {
+__device__ void fan_work(const FsArgs& a, uint32_t epoch, size_t act_off, int nv, int warps_per_cta) {
   constexpr int U = MoveCfg<V>::U;
   constexpr int SW = 32 * U;
   const int lane = threadIdx.x & 31;
-  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
-  // the planner records FS_ERANGE (and fs_check raises) when the rows exceed
-  // the buffer; never walk past it meanwhile
-  const long long rows_all = *reinterpret_cast<volatile int*>(a.num_rows);
-  const int rows = (int)(rows_all < a.max_rows ? rows_all : a.max_rows);
   const int S = (nv + SW - 1) / SW;
-  const int32_t* fs = reinterpret_cast<const int32_t*>(a.peer[a.rank] + fan_off);
+  unsigned long long* ctr = work_ctr(a, epoch, kWorkFanout);
+  const unsigned long long* ready = work_ctr(a, epoch, kWorkFanReady);
+  const unsigned long long* done = work_ctr(a, epoch, kWorkFanDone);
   V* act = reinterpret_cast<V*>(a.peer[a.rank] + act_off);
-  unsigned long long* cnt = work_ctr(a, epoch, kWorkFanout);
-  const uint32_t lt = (1u << lane) - 1u;
-  for (long long b = gw * 32; b < rows; b += nw * 32) {
-    const int r = (int)b + lane;
-    const int f = r < rows ? ld_cg(fs + r) : r;
-    const bool dup = r < rows && f != r && f >= 0 && f < rows;
-    const uint32_t m = __ballot_sync(kFull, dup);
-    if (m) {
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(cnt, (unsigned long long)__popc(m));
-      base = __shfl_sync(kFull, base, 0);
-      if (dup) a.fan_list[base + __popc(m & lt)] = make_int2(r, f);
+  const int2* dq = reinterpret_cast<const int2*>(a.peer[a.rank] + a.off_dupq);
+  const long long per_block = (long long)kBlockTokens * (a.K - 1);
+  unsigned long long seen = 0;  // last published word read by this warp
+  uint32_t k = 0;               // job of the previous unit (units are claimed in increasing order)
+  // balancer on: groups claimed dynamically; off: static striding over every warp
+  const unsigned long long wid = (unsigned long long)blockIdx.x * warps_per_cta + (threadIdx.x >> 5);
+  const unsigned long long nwk = (unsigned long long)gridDim.x * warps_per_cta;
+  unsigned long long grp = wid;
+  for (;; grp += nwk) {
+    const unsigned long long g0 = (a.balance ? (unsigned long long)claim_warp(ctr) : grp) * kFanGroup;
+    for (int gi = 0; gi < kFanGroup; ++gi) {
+      const unsigned long long u = g0 + gi;
+      // wait until the published prefix covers u (or every job is in)
+      unsigned backoff = 64;
+      while (u >= (seen & kUnitMask)) {
+        // lane 0 polls (with backoff: thousands of warps may wait here)
+        unsigned long long w = 0, d = 0;
+        if (lane == 0) {
+          d = ld_acquire_gpu_u64(done);
+          w = ld_acquire_gpu_u64(ready);
+        }
+        w = __shfl_sync(kFull, w, 0);
+        d = __shfl_sync(kFull, d, 0);
+        seen = w;
+        if (u < (seen & kUnitMask)) break;
+        if (d) return;  // final prefix read after `done`: u is past the last unit
+        __nanosleep(backoff);
+        backoff = backoff < 1024 ? backoff * 2 : 1024;
+      }
+      // job holding u: first k' >= k with jcum[k'] > u (lane-parallel window)
+      const uint32_t npub = (uint32_t)(seen >> 40);
+      while (k < npub) {
+        const uint32_t kk = k + lane;
+        const bool past = kk < npub && __ldcg(a.fan_jcum + kk) > u;
+        const uint32_t m = __ballot_sync(kFull, past);
+        if (m) {
+          k += __ffs(m) - 1;
+          break;
+        }
+        k += 32;
+      }
+      if (k >= npub) {  // cannot happen (jcum[npub-1] is the published total > u): fail loudly, never spin
+        if (lane == 0) record_error(a.status, FS_ERANGE);
+        return;
+      }
+      const unsigned long long base = k ? __ldcg(a.fan_jcum + k - 1) : 0ull;
+      const uint32_t jo = __ldcg(a.fan_jorder + k);
+      const int q = (int)(jo >> 16), b = (int)(jo & 0xffffu);
+      const unsigned long long loc = u - base;
+      const int entry = (int)(loc / (unsigned)S), sl = (int)(loc - (unsigned long long)entry * S);
+      const int2 rp = __ldcg(dq + (size_t)q * a.dupq_cap + (size_t)b * per_block + entry);
+      if (rp.x < 0 || rp.x >= a.max_rows || rp.y < 0 || rp.y >= a.max_rows) {
+        if (lane == 0) record_error(a.status, FS_ERANGE);
+        continue;
+      }
+      const int w0 = sl * SW, rem = nv - w0;
+      const V* src = act + (size_t)rp.y * nv + w0;
+      V* dst = act + (size_t)rp.x * nv + w0;
+      V v[U];
+#pragma unroll
+      for (int jj = 0; jj < U; ++jj)
+        if (jj * 32 + lane < rem) v[jj] = ld_cg(src + jj * 32 + lane);
+#pragma unroll
+      for (int jj = 0; jj < U; ++jj)
+        if (jj * 32 + lane < rem) st_na(dst + jj * 32 + lane, v[jj]);
     }
-  }
-  cg::this_grid().sync();
-  const uint32_t units = (uint32_t)*reinterpret_cast<volatile unsigned long long*>(cnt) * (uint32_t)S;
-  for (uint32_t u = (uint32_t)gw; u < units; u += (uint32_t)nw) {
-    const uint32_t ri = u / (uint32_t)S;
-    const int2 rf = __ldcg(a.fan_list + ri);
-    const int w0 = (int)(u - ri * (uint32_t)S) * SW, rem = nv - w0;
-    const V* src = act + (size_t)rf.y * nv + w0;
-    V* dst = act + (size_t)rf.x * nv + w0;
-    V v[U];
-#pragma unroll
-    for (int j = 0; j < U; ++j)
-      if (j * 32 + lane < rem) v[j] = ld_cg(src + j * 32 + lane);
-#pragma unroll
-    for (int j = 0; j < U; ++j)
-      if (j * 32 + lane < rem) st_na(dst + j * 32 + lane, v[j]);
   }
 }
 
@@ -135,39 +266,45 @@ __global__ void __launch_bounds__(kMoveThreads)
   const int nv = a.tb / (int)sizeof(V);
   const int S = (nv + SW - 1) / SW;
   const int lane = threadIdx.x & 31;
-  const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  const int wcta = threadIdx.x >> 5;
+  constexpr int kWarps = kMoveThreads / 32;
+  // roles: CTA 0's last warp watches the block words; warps below push_warps
+  // push first; the others fan out from the start (LOCAL-only launches: all push)
+  const bool remote = (phase & FS_PHASE_REMOTE) && P > 1;
+  const bool watcher = remote && blockIdx.x == 0 && wcta == kWarps - 1;
+  const bool pusher = (phase & FS_PHASE_LOCAL) && !watcher && (!remote || wcta < a.push_warps);
   __shared__ int32_t owner_sm[kMaxExperts];
   if (phase & FS_PHASE_LOCAL) load_owner_table(a, owner_sm);  // static table: before the PDL wait
   griddep_wait();  // row_of / the epoch come from the planner
   const uint32_t epoch = load_epoch(a);
-  const int parity = (int)(epoch & 1u);
   const size_t act_off = a.off_act;
-  const size_t fan_off = a.off_fansrc + (size_t)parity * a.fansrc_stride;
   trace_stamp(a, FS_TRACE_DISPATCH_BEGIN);
 
-  if (phase & FS_PHASE_LOCAL) {
-    const long long units = (long long)T * S;
+  if (pusher) {
+    // A claim is one (token, slice) unit, or a whole token (all S slices)
+    // with a.claim_tokens: fewer claims and one completion count per token,
+    // at the price of a coarser dynamic balance.
     const uint32_t uS = (uint32_t)S;
+    const uint32_t G = a.claim_tokens ? uS : 1u;  // units per claim
+    const long long claims = a.claim_tokens ? (long long)T : (long long)T * S;
     unsigned long long* ctr = work_ctr(a, epoch, kWorkDispatch);
-    long long u = claim_warp(ctr);
-    KMeta nxt = u < units ? load_meta(a, idx, row_of, (int)((uint32_t)u / uS), lane) : KMeta{0, -1};
-    while (u < units) {
-      const int i = (int)((uint32_t)u / uS);
-      const int sl = (int)((uint32_t)u - (uint32_t)i * uS);
+    // balancer on: claims taken dynamically (warps that drew light tokens
+    // take more); off: static striding over the pushing warps
+    const bool dyn = a.balance != 0;
+    const int npw = remote ? a.push_warps : kWarps;
+    const bool wexcl = remote && a.push_warps == kWarps;  // CTA 0's last warp watches instead
+    const long long pidx = (long long)blockIdx.x * npw + wcta - ((wexcl && blockIdx.x > 0) ? 1 : 0);
+    const long long pnum = (long long)gridDim.x * npw - (wexcl ? 1 : 0);
+    auto token_of = [&](long long c) { return (int)(G == uS ? (uint32_t)c : (uint32_t)c / uS); };
+    long long c = dyn ? claim_warp(ctr) : pidx;
+    KMeta nxt = c < claims ? load_meta(a, idx, row_of, token_of(c), lane) : KMeta{0, -1};
+    while (c < claims) {
+      const int i = token_of(c);
+      const int sl0 = G == uS ? 0 : (int)((uint32_t)c - (uint32_t)i * uS);
       const KMeta cur = nxt;
-      const long long un = claim_warp(ctr);  // next unit: claimed and prefetched during this one
-      if (un < units) nxt = load_meta(a, idx, row_of, (int)((uint32_t)un / uS), lane);
-      // payload loads first: they do not depend on the destinations
-      const int w0 = sl * SW;
-      const V* src = x + (size_t)i * nv + w0;
-      const int rem = nv - w0;
-      V v[U];
-#pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const int w = j * 32 + lane;
-        if (w < rem) v[j] = ld_nc(src + w);
-      }
+      const long long cn = dyn ? claim_warp(ctr) : c + pnum;  // next claim: taken and prefetched now
+      if (cn < claims) nxt = load_meta(a, idx, row_of, token_of(cn), lane);
+      // destinations of the token (lane k < K: owner and row of its k-th expert)
       int g = -1 - lane, r = -1;  // lanes >= K get unique negative keys
       if (lane < K) {
         g = owner_sm[cur.e];
@@ -178,41 +315,56 @@ __global__ void __launch_bounds__(kMoveThreads)
       const int r_first = __shfl_sync(kFull, r, first_lane);
       const bool direct = lane < K && r >= 0 && (a.nodedup || first_lane == lane || g == s);
       const uint32_t dmask = __ballot_sync(kFull, direct);
-      if (sl == 0 && lane < K && r >= 0) {
-        int32_t* fs = reinterpret_cast<int32_t*>(a.peer[g] + fan_off);
-        fs[r] = direct ? r : r_first;
-      }
+      const int b = i / kBlockTokens;
+      // a further row of the token on an already-reached rank: listed for the
+      // receiver's fan-out instead of crossing the link again
+      if (P > 1 && sl0 == 0 && lane < K && r >= 0 && !direct && r_first >= 0)
+        list_duplicate(a, epoch, g, b, r, r_first);
       // Rotate the destination order by token so concurrent warps of this
       // rank spread their first stores over different peers.
-      uint32_t m = dmask;
-      const int rot = (i + s) % K;
-      m = (m >> rot) | (rot ? (m << (32 - rot)) : 0u);
-      while (m) {
-        const int d0 = __ffs(m) - 1;
-        m &= m - 1;
-        const int d = (d0 + rot) & 31;
-        const int gd = __shfl_sync(kFull, g, d);
-        const int rd = __shfl_sync(kFull, r, d);
-        V* dst = reinterpret_cast<V*>(a.peer[gd] + act_off) + (size_t)rd * nv + w0;
+      const int rot = dyn ? (i + s) % K : 0;
+      const uint32_t mrot = (dmask >> rot) | (rot ? (dmask << (32 - rot)) : 0u);
+      for (int sl = sl0; sl < sl0 + (int)G; ++sl) {
+        // payload loads first: they do not depend on the destinations
+        const int w0 = sl * SW;
+        const V* src = x + (size_t)i * nv + w0;
+        const int rem = nv - w0;
+        V v[U];
 #pragma unroll
         for (int j = 0; j < U; ++j) {
           const int w = j * 32 + lane;
-          if (w < rem) st_na(dst + w, v[j]);
+          if (w < rem) v[j] = ld_nc(src + w);
+        }
+        uint32_t m = mrot;
+        while (m) {
+          const int d0 = __ffs(m) - 1;
+          m &= m - 1;
+          const int d = (d0 + rot) & 31;
+          const int gd = __shfl_sync(kFull, g, d);
+          const int rd = __shfl_sync(kFull, r, d);
+          V* dst = reinterpret_cast<V*>(a.peer[gd] + act_off) + (size_t)rd * nv + w0;
+#pragma unroll
+          for (int j = 0; j < U; ++j) {
+            const int w = j * 32 + lane;
+            if (w < rem) st_na(dst + w, v[j]);
+          }
         }
       }
-      u = un;
+      if (P > 1) {  // completion accounting of the claim's block
+        __syncwarp();
+        if (lane == 0) {
+          const int nt = min(kBlockTokens, T - b * kBlockTokens);
+          block_units_done(a, epoch, b, G, (uint32_t)(nt * S));
+        }
+      }
+      c = cn;
     }
-    if (P > 1) signal_pushed(a, epoch);
   }
   griddep_launch_dependents();  // the combine may start its prologue
-
   trace_stamp(a, FS_TRACE_DISPATCH_PUSHED);
-  if ((phase & FS_PHASE_REMOTE) && P > 1) {
-    if (threadIdx.x < P)
-      wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffArrive) + threadIdx.x, epoch, a);
-    __syncthreads();
-    trace_stamp(a, FS_TRACE_DISPATCH_ARRIVED);
-    fan_out_rows<V>(a, act_off, fan_off, nv, epoch);
+  if (remote) {
+    if (watcher) fan_watch(a, epoch, S);
+    fan_work<V>(a, epoch, act_off, nv, kWarps);
   }
   trace_stamp(a, FS_TRACE_DISPATCH_END);
 }
@@ -268,12 +420,11 @@ __global__ void __launch_bounds__(kTmaThreads)
   }
   griddep_wait();  // row_of / the epoch come from the planner
   const uint32_t epoch = load_epoch(a);
-  const int parity = (int)(epoch & 1u);
   const size_t act_off = a.off_act;
-  const size_t fan_off = a.off_fansrc + (size_t)parity * a.fansrc_stride;
   trace_stamp(a, FS_TRACE_DISPATCH_BEGIN);
+  const bool remote = (phase & FS_PHASE_REMOTE) && P > 1;
 
-  if (phase & FS_PHASE_LOCAL) {
+  if ((phase & FS_PHASE_LOCAL) && warp < 2) {
     if (warp == 0) {
       if (lane == 0) {  // producer (the first nslots rows were issued in the prologue)
         int n = 0;
@@ -301,10 +452,8 @@ __global__ void __launch_bounds__(kTmaThreads)
         const int first_lane = __ffs(same) - 1;
         const int r_first = __shfl_sync(kFull, r, first_lane);
         const bool direct = lane < K && r >= 0 && (a.nodedup || first_lane == lane || g == s);
-        if (lane < K && r >= 0) {
-          int32_t* fs = reinterpret_cast<int32_t*>(a.peer[g] + fan_off);
-          fs[r] = direct ? r : r_first;
-        }
+        if (P > 1 && lane < K && r >= 0 && !direct && r_first >= 0)
+          list_duplicate(a, epoch, g, i / kBlockTokens, r, r_first);
         mbar_wait(&full[q], (n / nslots) & 1);
         // each destination lane issues its own bulk store (per-thread bulk
         // groups); every lane commits one group per token so the lag below
@@ -319,17 +468,37 @@ __global__ void __launch_bounds__(kTmaThreads)
       bulk_wait<0>();
       fence_proxy_async_global();
     }
-    if (P > 1) signal_pushed(a, epoch);
+    if (P > 1) {
+      // every bulk store of this CTA is complete: count its tokens into their
+      // blocks (one unit per token; tokens are strided over the grid, so the
+      // blocks complete when the last CTA gets here)
+      asm volatile("bar.sync 1, 64;" ::: "memory");  // warps 0-1 only: the others may be fanning out
+      if (threadIdx.x == 0) {
+        auto flush = [&](int b, uint32_t n) {
+          block_units_done(a, epoch, b, n, (uint32_t)min(kBlockTokens, T - b * kBlockTokens));
+        };
+        int b_cur = -1;
+        uint32_t cnt = 0;
+        for (int i = blockIdx.x; i < T; i += gridDim.x) {
+          const int b = i / kBlockTokens;
+          if (b != b_cur) {
+            if (cnt) flush(b_cur, cnt);
+            b_cur = b;
+            cnt = 0;
+          }
+          ++cnt;
+        }
+        if (cnt) flush(b_cur, cnt);
+      }
+    }
   }
   griddep_launch_dependents();  // the combine may start its prologue
 
   trace_stamp(a, FS_TRACE_DISPATCH_PUSHED);
-  if ((phase & FS_PHASE_REMOTE) && P > 1) {
-    if (threadIdx.x < P)
-      wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffArrive) + threadIdx.x, epoch, a);
-    __syncthreads();
-    trace_stamp(a, FS_TRACE_DISPATCH_ARRIVED);
-    fan_out_rows<int4>(a, act_off, fan_off, tb / 16, epoch);
+  if (remote) {  // watcher: CTA 0's warp 3; every warp fans out once it has no push work
+    if (blockIdx.x == 0 && warp == 3) fan_watch(a, epoch, (tb / 16 + MoveCfg<int4>::kSliceWords - 1) /
+                                                              MoveCfg<int4>::kSliceWords);
+    fan_work<int4>(a, epoch, act_off, tb / 16, kTmaThreads / 32);
   }
   trace_stamp(a, FS_TRACE_DISPATCH_END);
 }

@@ -34,16 +34,24 @@ int fail(int code, const std::string& msg) {
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct RegionLayout {
-  size_t off_count, count_stride, off_fansrc, fansrc_stride, off_act, act_stride, off_actout, total;
+  size_t off_count, count_stride, off_blkflag, off_dupq, off_act, act_stride, off_actout, total;
+  int nbmax;
+  long long dupq_cap;
 };
 
-RegionLayout region_layout(int world, int E, int tb, long long max_rows, int with_act_out) {
+int blocks_per_source(int max_tokens) { return std::max(1, (max_tokens + kBlockTokens - 1) / kBlockTokens); }
+
+RegionLayout region_layout(int world, int E, int K, int tb, int max_tokens, long long max_rows, int with_act_out) {
   RegionLayout L;
+  L.nbmax = blocks_per_source(max_tokens);
+  L.dupq_cap = (long long)std::max(max_tokens, 0) * (K - 1);
   L.off_count = kSigBytes;
-  L.count_stride = align256((size_t)world * E * sizeof(uint64_t));  // epoch-tagged words
-  L.off_fansrc = L.off_count + 2 * L.count_stride;
-  L.fansrc_stride = align256((size_t)max_rows * sizeof(int32_t));
-  L.off_act = L.off_fansrc + 2 * L.fansrc_stride;
+  // epoch-tagged words: E per-expert counts + the source's token count
+  L.count_stride = align256((size_t)world * (E + 1) * sizeof(uint64_t));
+  L.off_blkflag = L.off_count + 2 * L.count_stride;
+  // block words [source][block] and duplicate lists [source][max_tokens * (K-1)]
+  L.off_dupq = L.off_blkflag + align256((size_t)world * L.nbmax * sizeof(uint64_t));
+  L.off_act = L.off_dupq + align256((size_t)world * (size_t)L.dupq_cap * sizeof(int2));
   L.act_stride = align256((size_t)max_rows * (size_t)tb);
   // one activation buffer: a rank's next dispatch cannot start before every
   // rank has published the next epoch's counts, i.e. finished this combine
@@ -68,6 +76,7 @@ struct fs_ctx {
   int pdl;              // 1: programmatic dependent launch planner -> dispatch (FUSCO_PDL=0 disables)
   int pdl_multi;        // 1: PDL for the cooperative P > 1 movers too (FUSCO_PDL_MULTI=0 disables)
   int nodedup;          // 1: no per-rank dedup on dispatch (FUSCO_NODEDUP=1; planner ablation)
+  int balance;          // 1: dynamic claiming + rotation (default); 0: static striding (balancer ablation)
   int cluster_layout;   // 1: single-cluster DSMEM planner usable (E <= 256, K <= 8)
   size_t cluster_smem;
   int combine_tma;      // 1: TMA combine engine (FUSCO_COMBINE=tma)
@@ -87,8 +96,13 @@ struct fs_ctx {
   int* status_d;
   int* num_rows_d;
   uint32_t* epoch_d;  // device iteration counter (graph-replay safe)
-  unsigned long long* work_d;  // [2][8] dynamic work counters
-  int2* fan_list_d;            // [max_rows] fan-out list (P > 1)
+  unsigned long long* work_d;  // [2][8][kWorkStride] dynamic work counters
+  uint32_t *blkdone_d, *dupcnt_d;  // [2][nbmax], [2][P][nbmax] dispatch block accounting (P > 1)
+  unsigned long long* jcum_d;      // [P * nbmax] receiver fan-out schedule
+  uint32_t* jorder_d;              // [P * nbmax]
+  int push_warps;                  // warps per dispatch CTA that push before fanning out
+  int claim_tokens;                // dispatch claim granularity: 1 = whole tokens, 0 = (token, slice) units
+  int disp_ctas_per_sm;            // P > 1 warp-mover grid cap (0 = occupancy)
   unsigned long long* trace_d;  // FS_NTRACE stamps when FUSCO_TRACE=1, else null
 };
 
@@ -105,6 +119,7 @@ FsArgs make_args(const fs_ctx* h, int T, int idx64) {
   a.T = T;
   a.idx64 = idx64;
   a.nodedup = h->nodedup;
+  a.balance = h->balance;
   a.epoch_ptr = h->epoch_d;
   a.max_rows = h->max_rows;
   a.owner = h->owner_d;
@@ -113,12 +128,20 @@ FsArgs make_args(const fs_ctx* h, int T, int idx64) {
   a.seg_begin = h->seg_d;
   for (int g = 0; g < h->world; ++g) a.peer[g] = h->peers[g];
   a.off_count = h->L.off_count;
-  a.off_fansrc = h->L.off_fansrc;
+  a.off_blkflag = h->L.off_blkflag;
+  a.off_dupq = h->L.off_dupq;
   a.off_act = h->L.off_act;
   a.off_actout = h->L.off_actout;
   a.count_stride = h->L.count_stride;
-  a.fansrc_stride = h->L.fansrc_stride;
   a.act_stride = h->L.act_stride;
+  a.nbmax = h->L.nbmax;
+  a.dupq_cap = h->L.dupq_cap;
+  a.push_warps = h->push_warps;
+  a.claim_tokens = h->claim_tokens;
+  a.blkdone = h->blkdone_d;
+  a.dupcnt = h->dupcnt_d;
+  a.fan_jcum = h->jcum_d;
+  a.fan_jorder = h->jorder_d;
   a.chunk_cnt = h->chunk_cnt_d;
   a.totals = h->totals_d;
   a.stat_part = h->stat_part_d;
@@ -127,7 +150,6 @@ FsArgs make_args(const fs_ctx* h, int T, int idx64) {
   a.timeout_ns = h->timeout_ns;
   a.trace = h->trace_d;
   a.work = h->work_d;
-  a.fan_list = h->fan_list_d;
   return a;
 }
 
@@ -180,12 +202,12 @@ int fs_abi_version(void) { return FS_ABI_VERSION; }
 
 const char* fs_last_error(void) { return g_err.c_str(); }
 
-int fs_region_bytes(int world, int num_experts, int token_bytes, long long max_rows, int with_act_out,
-                    size_t* bytes_out) {
-  if (!bytes_out || world < 1 || world > FS_MAX_RANKS || num_experts < 1 || token_bytes <= 0 ||
-      max_rows < 0)
+int fs_region_bytes(int world, int num_experts, int topk, int token_bytes, int max_tokens, long long max_rows,
+                    int with_act_out, size_t* bytes_out) {
+  if (!bytes_out || world < 1 || world > FS_MAX_RANKS || num_experts < 1 || topk < 1 || token_bytes <= 0 ||
+      max_tokens < 0 || max_rows < 0)
     return fail(FS_EINVAL, "fs_region_bytes: bad arguments");
-  *bytes_out = region_layout(world, num_experts, token_bytes, max_rows, with_act_out).total;
+  *bytes_out = region_layout(world, num_experts, topk, token_bytes, max_tokens, max_rows, with_act_out).total;
   return FS_OK;
 }
 
@@ -287,7 +309,7 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
   h->nloc = seg[rank + 1] - seg[rank];
   h->epoch = 0;
   h->timeout_ns = (unsigned long long)(timeout_ms > 0 ? timeout_ms : 10000) * 1000000ull;
-  h->L = region_layout(world, num_experts, token_bytes, max_rows, h->with_act_out);
+  h->L = region_layout(world, num_experts, topk, token_bytes, max_tokens, max_rows, h->with_act_out);
   h->peers.assign((char* const*)peer_regions, (char* const*)peer_regions + world);
   h->layout_smem = layout_smem_bytes(num_experts, topk);
   auto cleanup = [&](int rc) {
@@ -353,8 +375,18 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
   }
   h->sms = sms;
   {
+    // dispatch warps per CTA that push before fanning out (P > 1; the others
+    // fan out duplicates from the start): FUSCO_PUSH_WARPS, default all
+    const char* pw = getenv("FUSCO_PUSH_WARPS");
+    h->push_warps = pw ? std::max(1, std::min(kMoveThreads / 32, atoi(pw))) : kMoveThreads / 32;
+    const char* cl = getenv("FUSCO_CLAIM");  // unit | token
+    h->claim_tokens = cl && std::string(cl) == "token";
+    const char* dc = getenv("FUSCO_DISP_CTAS");  // P > 1 warp mover: CTAs per SM cap
+    h->disp_ctas_per_sm = dc ? std::max(1, std::min(kMaxCtasPerSm, atoi(dc))) : 0;
     const char* nd = getenv("FUSCO_NODEDUP");
     h->nodedup = nd && std::string(nd) == "1";
+    const char* bl = getenv("FUSCO_BALANCE");
+    h->balance = !(bl && std::string(bl) == "0");
     const char* pd = getenv("FUSCO_PDL");
     h->pdl = !(pd && std::string(pd) == "0");
     const char* pm = getenv("FUSCO_PDL_MULTI");
@@ -415,8 +447,11 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
       (e = dalloc((void**)&h->status_d, 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->num_rows_d, 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->epoch_d, 4)) != cudaSuccess ||
-      (e = dalloc((void**)&h->work_d, 2 * 8 * 8)) != cudaSuccess ||
-      (world > 1 && (e = dalloc((void**)&h->fan_list_d, (size_t)max_rows * sizeof(int2))) != cudaSuccess))
+      (e = dalloc((void**)&h->work_d, kWorkWords * 8)) != cudaSuccess ||
+      (e = dalloc((void**)&h->blkdone_d, (size_t)2 * h->L.nbmax * kBlkStride * 4)) != cudaSuccess ||
+      (e = dalloc((void**)&h->dupcnt_d, (size_t)2 * world * h->L.nbmax * 4)) != cudaSuccess ||
+      (e = dalloc((void**)&h->jcum_d, (size_t)world * h->L.nbmax * 8)) != cudaSuccess ||
+      (e = dalloc((void**)&h->jorder_d, (size_t)world * h->L.nbmax * 4)) != cudaSuccess)
     return cleanup(fail(FS_ECUDA, std::string("fs_create alloc: ") + cudaGetErrorString(e)));
   if ((e = cudaMemcpy(h->owner_d, owner.data(), num_experts * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(h->node_of_d, nodes.data(), world * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
@@ -425,9 +460,11 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
       (e = cudaMemset(h->status_d, 0, 4)) != cudaSuccess ||
       (e = cudaMemset(h->num_rows_d, 0, 4)) != cudaSuccess ||
       (e = cudaMemset(h->epoch_d, 0, 4)) != cudaSuccess ||
-      (e = cudaMemset(h->work_d, 0, 2 * 8 * 8)) != cudaSuccess ||
+      (e = cudaMemset(h->work_d, 0, kWorkWords * 8)) != cudaSuccess ||
       (e = cudaMemset(h->totals_d, 0, (size_t)2 * num_experts * 4)) != cudaSuccess ||
       (e = cudaMemset(h->stat_part_d, 0, (size_t)2 * 8 * 8)) != cudaSuccess ||
+      (e = cudaMemset(h->blkdone_d, 0, (size_t)2 * h->L.nbmax * kBlkStride * 4)) != cudaSuccess ||
+      (e = cudaMemset(h->dupcnt_d, 0, (size_t)2 * world * h->L.nbmax * 4)) != cudaSuccess ||
       (e = cudaDeviceSynchronize()) != cudaSuccess)
     return cleanup(fail(FS_ECUDA, std::string("fs_create init: ") + cudaGetErrorString(e)));
   {
@@ -456,7 +493,10 @@ int fs_destroy(fs_handle_t h) {
   cudaFree(h->num_rows_d);
   cudaFree(h->epoch_d);
   cudaFree(h->work_d);
-  if (h->fan_list_d) cudaFree(h->fan_list_d);
+  cudaFree(h->blkdone_d);
+  cudaFree(h->dupcnt_d);
+  cudaFree(h->jcum_d);
+  cudaFree(h->jorder_d);
   if (h->trace_d) cudaFree(h->trace_d);
   delete h;
   return FS_OK;
@@ -496,6 +536,13 @@ int fs_set_nodedup(fs_handle_t h, int on) {
   if (!h) return fail(FS_EINVAL, "null handle");
   if (on != 0 && on != 1) return fail(FS_EINVAL, "on must be 0 or 1");
   h->nodedup = on;
+  return FS_OK;
+}
+
+int fs_set_balance(fs_handle_t h, int on) {
+  if (!h) return fail(FS_EINVAL, "null handle");
+  if (on != 0 && on != 1) return fail(FS_EINVAL, "on must be 0 or 1");
+  h->balance = on;
   return FS_OK;
 }
 
@@ -594,7 +641,9 @@ int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_byte
   const long long slices = ((long long)h->tb / elem + 32 * U - 1) / (32 * U);
   const long long units = (long long)num_tokens * slices;
   const long long want = (units + kMoveThreads / 32 - 1) / (kMoveThreads / 32);
-  const int grid = (int)std::min<long long>(h->move_grid, std::max<long long>(want, h->sms));
+  int cap = h->move_grid;
+  if (h->world > 1 && h->disp_ctas_per_sm > 0) cap = std::min(cap, h->disp_ctas_per_sm * h->sms);
+  const int grid = (int)std::min<long long>(cap, std::max<long long>(want, h->sms));
   return launch_ex(fn, grid, kMoveThreads, 0, stream, args, true, h->pdl_multi);
 }
 
@@ -620,7 +669,8 @@ int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes, const int32_t
     // re-arm the dynamic item counter (both parities: the other one is the
     // next epoch's, zeroed by its planner anyway), stream-ordered and graph-safe
     for (int q = 0; q < 2; ++q)
-      FS_CUDA(cudaMemsetAsync(h->work_d + q * 8 + kWorkCombine, 0, sizeof(unsigned long long), (cudaStream_t)stream));
+      FS_CUDA(cudaMemsetAsync(h->work_d + ((size_t)q * kWorkSlots + kWorkCombine) * kWorkStride, 0,
+                              sizeof(unsigned long long), (cudaStream_t)stream));
   }
   h->comb_phases |= phase;
   FsArgs a = make_args(h, num_tokens, idx_bytes == 8);

@@ -26,13 +26,20 @@ constexpr int kMoveThreads = 256;  // dispatch / combine warp-mover CTA size
 constexpr size_t kSigBytes = 4096;
 constexpr size_t kOffCountFlag = 0;    // u32[FS_MAX_RANKS]: reserved (the counts are epoch-tagged words)
 constexpr size_t kOffReadyFlag = 256;  // u32[FS_MAX_RANKS]: expert outputs ready
-constexpr size_t kOffArrive = 512;     // u32[FS_MAX_RANKS]: source s finished pushing here (epoch)
-constexpr size_t kOffDone = 1024;      // u64: reserved
+
+// Completion blocks of the dispatch (P > 1): a source's tokens are cut into
+// blocks of kBlockTokens; when every unit of block b has been pushed, the
+// source releases one epoch-tagged word per destination rank carrying the
+// number of duplicate rows it listed there for that block, and the
+// destination fans those rows out while later blocks are still in flight.
+constexpr int kBlockTokens = 128;
+constexpr int kBlkStride = 32;  // u32 words per block counter (one 128-byte line each)
 
 struct FsArgs {
   int rank, world, E, K, tb, T;
   int idx64;      // topk_idx element size 8 (else 4)
   int nodedup;    // 1: every (token, k) row crosses the link (the reference's "planner" ablation)
+  int balance;    // 1 (default): dynamic work claiming + rotated destination order; 0: static striding
   // Iteration counter in device memory (per handle), so a captured CUDA graph
   // replays correctly: fs_layout's LOCAL phase uses *epoch + 1 and stores it;
   // every later phase/kernel of the iteration reads it.  parity = epoch & 1
@@ -44,8 +51,12 @@ struct FsArgs {
   const int32_t* perm;       // [E] experts sorted by (owner, id)
   const int32_t* seg_begin;  // [P+1] segment of rank g in perm
   char* peer[FS_MAX_RANKS];  // every rank's region, mapped here
-  size_t off_count, off_fansrc, off_act, off_actout;
-  size_t count_stride, fansrc_stride, act_stride;  // bytes per parity copy
+  size_t off_count, off_blkflag, off_dupq, off_act, off_actout;
+  size_t count_stride, act_stride;  // bytes per parity copy
+  int nbmax;                 // completion blocks per source (ceil(max_tokens / kBlockTokens))
+  long long dupq_cap;        // duplicate-list entries per source in a region (max_tokens * (K - 1))
+  int push_warps;            // warps per CTA that push first (the rest fan out from the start)
+  int claim_tokens;          // 1: pushers claim whole tokens (all slices), 0: (token, slice) units
   int32_t* chunk_cnt;        // [chunks][E] scratch (per handle)
   int32_t* totals;           // [2][E] per-parity per-expert atomic totals (per handle)
   long long* stat_part;      // [2][8] per-parity atomic statistics accumulators
@@ -53,15 +64,26 @@ struct FsArgs {
   int* num_rows;             // rows of the own activation buffer this epoch
   unsigned long long timeout_ns;
   unsigned long long* trace;  // optional globaltimer stamps (FUSCO_TRACE=1), see FS_TRACE_*
-  unsigned long long* work;   // [2][8] per-parity dynamic work counters (zeroed one epoch ahead)
-  int2* fan_list;             // [max_rows] receiver fan-out list (row, primary row), P > 1
+  unsigned long long* work;   // [2][8][kWorkStride] per-parity dynamic work counters (zeroed one epoch ahead)
+  // sender-side block accounting, per parity (zeroed one epoch ahead by the planner)
+  uint32_t* blkdone;          // [2][nbmax][kBlkStride] units of block b pushed (word 0 of a line)
+  uint32_t* dupcnt;           // [2][P][nbmax] duplicate rows listed at rank g for block b
+  // receiver-side fan-out schedule (this epoch): published jobs in arrival order
+  unsigned long long* fan_jcum;  // [P * nbmax] cumulative fan-out units after job k
+  uint32_t* fan_jorder;          // [P * nbmax] job k = (source << 16) | block
 };
 
 // dynamic work counters (slot within work[parity][*])
 constexpr int kWorkDispatch = 0;
-constexpr int kWorkFanout = 1;
+constexpr int kWorkFanout = 1;    // fan-out unit claims (groups of kFanGroup units)
 constexpr int kWorkCombine = 2;
-constexpr int kWorkDone = 3;  // dispatch CTAs of this epoch done pushing (target gridDim.x)
+constexpr int kWorkFanReady = 4;  // (published jobs << 40) | published fan-out units
+constexpr int kWorkFanDone = 5;   // every job published (or the wait timed out)
+constexpr int kWorkSlots = 8;
+// one 128-byte line per counter: the words fan-out workers poll must not
+// share a line with the counters pushers claim from
+constexpr int kWorkStride = 16;
+constexpr size_t kWorkWords = 2 * kWorkSlots * kWorkStride;  // [2 parities][8 slots][16]
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -150,13 +172,33 @@ __device__ __forceinline__ bool wait_u64_geq(const unsigned long long* p, unsign
 // Each word of the P x E count matrix carries (epoch << 32 | count): a reader
 // polls the words themselves, so the publisher needs neither a release fence
 // nor a separate flag (one NVLink traversal instead of data + fence + flag).
+// Row s of the matrix has E + 1 words: the per-expert counts, then the
+// source's token count (the receiver's dispatch derives its blocks from it).
 __device__ __forceinline__ void publish_count(const FsArgs& a, int parity, uint32_t epoch, int e, int count) {
   const unsigned long long w = ((unsigned long long)epoch << 32) | (uint32_t)count;
   for (int g = 0; g < a.world; ++g) {
     unsigned long long* m =
         reinterpret_cast<unsigned long long*>(a.peer[g] + a.off_count + (size_t)parity * a.count_stride);
-    st_relaxed_sys_u64(m + (size_t)a.rank * a.E + e, w);
+    st_relaxed_sys_u64(m + (size_t)a.rank * (a.E + 1) + e, w);
   }
+}
+// One epoch-tagged count word of source q (waits for this epoch's value).
+__device__ __forceinline__ int read_count_word(const FsArgs& a, int parity, uint32_t epoch, int q, int e) {
+  const unsigned long long* p = reinterpret_cast<const unsigned long long*>(
+                                    a.peer[a.rank] + a.off_count + (size_t)parity * a.count_stride) +
+                                (size_t)q * (a.E + 1) + e;
+  unsigned long long w = ld_acquire_sys_u64(p);
+  if ((uint32_t)(w >> 32) != epoch) {
+    const unsigned long long t0 = globaltimer();
+    do {
+      if (globaltimer() - t0 > a.timeout_ns) {
+        record_error(a.status, FS_ETIMEOUT);
+        return 0;
+      }
+      w = ld_acquire_sys_u64(p);
+    } while ((uint32_t)(w >> 32) != epoch);
+  }
+  return (int)(uint32_t)w;
 }
 // Σ_q cnt[q][e] and Σ_{q<rank} cnt[q][e] from this rank's matrix, waiting for
 // every source's word of this epoch.
@@ -166,7 +208,7 @@ __device__ __forceinline__ void gather_counts(const FsArgs& a, int parity, uint3
       reinterpret_cast<const unsigned long long*>(a.peer[a.rank] + a.off_count + (size_t)parity * a.count_stride);
   int t = 0, b = 0;
   for (int q = 0; q < a.world; ++q) {
-    const unsigned long long* p = m + (size_t)q * a.E + e;
+    const unsigned long long* p = m + (size_t)q * (a.E + 1) + e;
     unsigned long long w = ld_acquire_sys_u64(p);
     if ((uint32_t)(w >> 32) != epoch) {
       const unsigned long long t0 = globaltimer();
@@ -186,26 +228,54 @@ __device__ __forceinline__ void gather_counts(const FsArgs& a, int parity, uint3
   *before = b;
 }
 
-// End of a rank's push phase: every CTA makes its peer stores visible at
-// system scope (bar.sync, then one fence.acq_rel.sys by thread 0) and counts
-// itself done on a local counter; the last CTA of the epoch then releases
-// one flag per peer (value = epoch).  One NVLink signal per (source,
-// destination) instead of one per CTA.
-__device__ __forceinline__ void signal_pushed(const FsArgs& a, uint32_t epoch) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    // per-parity counter, zeroed by the planner for the next epoch, so the
-    // grid may differ between launches
-    unsigned long long* done = a.work + (size_t)(epoch & 1u) * 8 + kWorkDone;
-    const unsigned long long prev = atom_add_acq_rel_gpu_u64(done, 1ull);
-    if (prev + 1 == (unsigned long long)gridDim.x) {
-      if (a.trace != nullptr) a.trace[7] = globaltimer();  // the last CTA's signal
-      for (int g = 0; g < a.world; ++g)
-        st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[g] + kOffArrive) + a.rank, epoch);
-    }
+// ---- completion blocks (sender side) -----------------------------------
+// A unit (or a CTA's batch of units) of block b is done: count it on the
+// block's local counter with acq_rel at gpu scope (cumulative over the
+// caller's peer stores, which precede it in program / barrier order).  The
+// arrival that completes the block has acquired every other unit's release;
+// it issues one fence.sc.sys (so every one of the block's NVLink stores is
+// ordered before what follows at system scope) and releases the block word
+// on each destination: (epoch << 32) | number of duplicate-list entries it
+// holds.  One flag per (source, destination, block) instead of one per unit
+// — a per-unit system fence waits for the deep NVLink store queue and was
+// measured slower.
+__device__ __forceinline__ uint32_t atom_add_acq_rel_gpu_u32(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_gpu_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long* blkflag_ptr(const FsArgs& a, int g, int src, int b) {
+  return reinterpret_cast<unsigned long long*>(a.peer[g] + a.off_blkflag) + (size_t)src * a.nbmax + b;
+}
+__device__ __forceinline__ void block_units_done(const FsArgs& a, uint32_t epoch, int b, uint32_t n,
+                                                 uint32_t total) {
+  const int par = (int)(epoch & 1u);
+  const uint32_t prev = atom_add_acq_rel_gpu_u32(a.blkdone + ((size_t)par * a.nbmax + b) * kBlkStride, n);
+  if (prev + n != total) return;
+  __threadfence_system();
+  for (int g = 0; g < a.world; ++g) {
+    if (g == a.rank) continue;
+    const uint32_t nd = ld_relaxed_gpu_u32(a.dupcnt + ((size_t)par * a.world + g) * a.nbmax + b);
+    st_release_sys_u64(blkflag_ptr(a, g, a.rank, b), ((unsigned long long)epoch << 32) | nd);
   }
 }
+// Duplicate-list entry of (dup row, primary row) on rank g for block b.
+__device__ __forceinline__ void list_duplicate(const FsArgs& a, uint32_t epoch, int g, int b, int row, int prim) {
+  uint32_t* cnt = a.dupcnt + ((size_t)(epoch & 1u) * a.world + g) * a.nbmax + b;
+  const uint32_t slot = atomicAdd(cnt, 1u);
+  int2* q = reinterpret_cast<int2*>(a.peer[g] + a.off_dupq) + (size_t)a.rank * a.dupq_cap +
+            (size_t)b * kBlockTokens * (a.K - 1) + slot;
+  *q = make_int2(row, prim);
+}
+
 // ---- 16-byte / 4-byte vector moves ----------------------------------------
 // Read-only inputs (x, peers' finished act/act_out): non-coherent path, no L1
 // allocation (streaming).  Data written by peers inside the same kernel
@@ -270,7 +340,7 @@ __device__ __forceinline__ long long claim_warp(unsigned long long* ctr) {
   return (long long)__shfl_sync(0xffffffffu, v, 0);
 }
 __device__ __forceinline__ unsigned long long* work_ctr(const FsArgs& a, uint32_t epoch, int slot) {
-  return a.work + (size_t)(epoch & 1u) * 8 + slot;
+  return a.work + ((size_t)(epoch & 1u) * kWorkSlots + slot) * kWorkStride;
 }
 
 __device__ __forceinline__ uint32_t load_epoch(const FsArgs& a) {

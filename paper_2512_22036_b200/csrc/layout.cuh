@@ -103,6 +103,17 @@ __device__ __forceinline__ void chunk_prefix(const int32_t* cnt, int n, int E, i
   }
 }
 
+// The next epoch's dispatch block counters (sender side, P > 1): zeroed one
+// epoch ahead, like the work counters.
+__device__ __forceinline__ void zero_next_blocks(const FsArgs& a, int parity, int tid, int nthreads) {
+  if (a.world == 1) return;
+  const int nb = a.nbmax;
+  uint32_t* done = a.blkdone + (size_t)(parity ^ 1) * nb * kBlkStride;
+  uint32_t* dup = a.dupcnt + (size_t)(parity ^ 1) * a.world * nb;
+  for (int j = tid; j < nb; j += nthreads) done[(size_t)j * kBlkStride] = 0u;
+  for (int j = tid; j < a.world * nb; j += nthreads) dup[j] = 0u;
+}
+
 // ===========================================================================
 // Layout planner
 //
@@ -308,13 +319,14 @@ __global__ void __launch_bounds__(kLayoutThreads)
       int32_t* next_totals = a.totals + (size_t)(parity ^ 1) * E;
       long long* next_stats = a.stat_part + (parity ^ 1) * 8;
       if (P > 1)
-        for (int e = tid; e < E; e += kLayoutThreads)
-          publish_count(a, parity, epoch, e, single ? cnt_s[e] : ld_cg(totals + e));
+        for (int e = tid; e <= E; e += kLayoutThreads)
+          publish_count(a, parity, epoch, e, e == E ? T : (single ? cnt_s[e] : ld_cg(totals + e)));
       for (int e = tid; e < E; e += kLayoutThreads) next_totals[e] = 0;
+      zero_next_blocks(a, parity, tid, kLayoutThreads);
       if (stats && tid >= 5 && tid < FS_NSTATS) stats[tid] = 0;
       if (tid < 8) {
         next_stats[tid] = 0;
-        a.work[(size_t)(parity ^ 1) * 8 + tid] = 0ull;  // the next epoch's work counters
+        a.work[((size_t)(parity ^ 1) * kWorkSlots + tid) * kWorkStride] = 0ull;  // the next epoch's work counters
       }
       // every CTA read the old epoch before the grid barrier: safe to bump
       if (tid == 0) *a.epoch_ptr = epoch;
@@ -561,7 +573,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   __syncthreads();
   if (crank == 0) {
     if (P > 1)
-      for (int e = tid; e < E; e += kClusterThreads) publish_count(a, parity, epoch, e, tot[e]);
+      for (int e = tid; e <= E; e += kClusterThreads) publish_count(a, parity, epoch, e, e == E ? T : tot[e]);
+    zero_next_blocks(a, parity, tid, kClusterThreads);
     if (stats && tid < 4) {
       long long acc = 0;
       for (int r = 0; r < CS; ++r) {
@@ -580,7 +593,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     for (int e = tid; e < E; e += kClusterThreads) a.totals[(size_t)(parity ^ 1) * E + e] = 0;
     if (tid < 8) {
       a.stat_part[(parity ^ 1) * 8 + tid] = 0;
-      a.work[(size_t)(parity ^ 1) * 8 + tid] = 0ull;
+      a.work[((size_t)(parity ^ 1) * kWorkSlots + tid) * kWorkStride] = 0ull;
     }
     if (tid == 0) *a.epoch_ptr = epoch;  // every CTA read the old epoch before the cluster barrier
     trace_stamp(a, FS_TRACE_LAYOUT_PUBLISH);

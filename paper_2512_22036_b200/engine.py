@@ -128,6 +128,7 @@ class Rank:
         grid_ctas: int = 0,
         timeout_ms: int = 0,
         nodedup: bool = False,
+        balance: bool = True,
     ):
         self.device = torch.device(device)
         self.dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
@@ -150,6 +151,8 @@ class Rank:
         self.handle = h
         if nodedup:  # the reference's planner ablation: every (token, k) row crosses the link
             call("fs_set_nodedup", h, 1)
+        if not balance:  # the reference's balancer ablation: static work striding, no rotation
+            call("fs_set_balance", h, 0)
         self.with_act_out = bool(with_act_out)
         self.max_rows = int(_lib.load().fs_max_rows(h))
         self.region = regions[rank]
@@ -281,9 +284,11 @@ class Rank:
         call("fs_check", self.handle, stream_ptr(stream))
 
 
-def region_bytes(world: int, num_experts: int, token_bytes: int, max_rows: int, with_act_out: bool) -> int:
+def region_bytes(world: int, num_experts: int, topk: int, token_bytes: int, max_tokens: int, max_rows: int,
+                 with_act_out: bool) -> int:
     n = c_size_t()
-    call("fs_region_bytes", world, num_experts, token_bytes, int(max_rows), int(with_act_out), byref(n))
+    call("fs_region_bytes", world, num_experts, topk, token_bytes, max_tokens, int(max_rows), int(with_act_out),
+         byref(n))
     return n.value
 
 
@@ -313,6 +318,7 @@ class EmulatedCluster:
         device: torch.device | str | None = None,
         timeout_ms: int = 0,
         nodedup: bool = False,
+        balance: bool = True,
     ):
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         if self.device.index is None:
@@ -323,7 +329,7 @@ class EmulatedCluster:
         self.topk = topk
         self.owner = owner
         mr = max_rows or default_max_rows(world, max_tokens, topk, owner)
-        nbytes = region_bytes(world, num_experts, token_bytes, mr, with_act_out)
+        nbytes = region_bytes(world, num_experts, topk, token_bytes, max_tokens, mr, with_act_out)
         self.regions: list[int] = []
         for _ in range(world):
             p = c_void_p()
@@ -334,7 +340,7 @@ class EmulatedCluster:
                 device=self.device, rank=r, world=world, num_experts=num_experts, topk=topk,
                 token_bytes=token_bytes, max_tokens=max_tokens, owner=owner, node_of=node_of,
                 regions=self.regions, max_rows=mr, with_act_out=with_act_out, grid_ctas=grid_ctas,
-                timeout_ms=timeout_ms, nodedup=nodedup,
+                timeout_ms=timeout_ms, nodedup=nodedup, balance=balance,
             )
             for r in range(world)
         ]
@@ -424,6 +430,7 @@ class EPBuffer:
         grid_ctas: int = 0,
         timeout_ms: int = 0,
         exchange=None,
+        balance: bool = True,
     ):
         import torch.distributed as dist
 
@@ -441,7 +448,7 @@ class EPBuffer:
         token_bytes = hidden * elem
         owner = np.arange(num_experts) % self.world if owner is None else np.asarray(owner)
         mr = max_rows or default_max_rows(self.world, max_tokens, topk, owner)
-        nbytes = region_bytes(self.world, num_experts, token_bytes, mr, with_act_out)
+        nbytes = region_bytes(self.world, num_experts, topk, token_bytes, max_tokens, mr, with_act_out)
         cfg = (self.world, num_experts, topk, token_bytes, max_tokens, int(mr), bool(with_act_out),
                tuple(int(o) for o in owner), int(grid_ctas))
         own = c_void_p()
@@ -464,7 +471,7 @@ class EPBuffer:
                 device=self.device, rank=self.rank_id, world=self.world, num_experts=num_experts, topk=topk,
                 token_bytes=token_bytes, max_tokens=max_tokens, owner=owner, node_of=None,
                 regions=self._peers.regions, max_rows=mr, with_act_out=with_act_out, grid_ctas=grid_ctas,
-                timeout_ms=timeout_ms,
+                timeout_ms=timeout_ms, balance=balance,
             )
         except BaseException:  # release what was mapped / allocated before re-raising
             lib = _lib.load()

@@ -3,7 +3,8 @@
 Same cells (pattern x seq_len, seq_len = total tokens as the reference's
 ``generate(pattern, seq_len, ...)``, bench.py:128-132) and variants (fused, baseline =
 disaggregated pack/exchange/unpack, planner_off = no dedup, balancer_off =
-static groups) and the same row fields as the reference
+static groups and the device balancing off — static work striding, no
+rotation, ``fs_set_balance``) and the same row fields as the reference
 (``ROW_FIELDS``, bench.py:48-63), but the times are CUDA-event measurements
 of the kernels on one B200 with the P ranks emulated (``run_exchange``), plus
 ``latency_us``, ``routed_gbps`` (2·T·K·tb per round trip / time), ``hbm_gbps``
@@ -11,8 +12,9 @@ of the kernels on one B200 with the P ranks emulated (``run_exchange``), plus
 and ``roofline_frac`` (hbm_gbps / the measured HBM peak).  Rows are emitted as JSON (schema id
 ``fusco-b200/bench-result/1``, sha256 config fingerprint), CSV or Markdown.
 
-    python -m paper_2512_22036_b200.matrix --preset box8 --seq-lens 4096 8192 \
+    python -m paper_2512_22036_b200.matrix --topology box8 --seq-lens 4096 8192 \
         --variants fused baseline planner_off --format md
+    python -m paper_2512_22036_b200.matrix --topology topo.json --trace captured.json
 """
 
 from __future__ import annotations
@@ -28,8 +30,8 @@ from pathlib import Path
 
 import numpy as np
 
-from .routing import GENERATORS, generate
-from .topology import ClusterTopology, ExpertPlacement, preset
+from .routing import GENERATORS, RoutingAssignment, generate, load_trace
+from .topology import ClusterTopology, ExpertPlacement, load_topology, preset
 
 SCHEMA_ID = "fusco-b200/bench-result/1"
 ROW_FIELDS = (
@@ -56,6 +58,10 @@ class BenchConfig:
     seed: int = 0
     repeats: int = 3
     extra: dict = field(default_factory=dict)
+    # a recorded routing (reference bench.py:79-80, 123-130): replaces the
+    # generated patterns with one cell of the trace's tokens
+    trace: RoutingAssignment | None = None
+    trace_label: str = "trace"
 
     def fingerprint_doc(self) -> dict:
         return {
@@ -64,6 +70,7 @@ class BenchConfig:
             "patterns": list(self.patterns), "seq_lens": list(self.seq_lens), "topk": self.topk,
             "token_bytes": self.token_bytes, "dtype": self.dtype, "balancer": self.balancer,
             "variants": list(self.variants), "seed": self.seed, "repeats": self.repeats,
+            "trace": self.trace_label if self.trace is not None else None,
         }
 
     def fingerprint(self) -> str:
@@ -71,12 +78,16 @@ class BenchConfig:
 
 
 def cells(cfg: BenchConfig) -> list[tuple[str, int]]:
+    if cfg.trace is not None:
+        return [(cfg.trace_label, cfg.trace.num_tokens)]
     return [(p, s) for p in cfg.patterns for s in cfg.seq_lens]
 
 
 def cell_assignment(cfg: BenchConfig, index: int, pattern: str, seq_len: int):
     """Per-cell routing: seq_len tokens in total, SeedSequence((seed, index))
-    as the reference (bench.py:128-132)."""
+    as the reference (bench.py:128-132); the recorded trace when one is given."""
+    if cfg.trace is not None:
+        return cfg.trace
     rng = np.random.default_rng(np.random.SeedSequence((cfg.seed, index)))
     return generate(pattern, seq_len, cfg.topk, cfg.topo, cfg.placement, rng)
 
@@ -230,7 +241,10 @@ def render(doc: dict, fmt: str) -> str:
 
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
-    ap.add_argument("--preset", default="box8", help="topology preset: box8, test, large")
+    ap.add_argument("--topology", "--preset", dest="topology", default="box8",
+                    help="topology preset (box8, test, large) or path to a topology JSON file (bench.py:291-298)")
+    ap.add_argument("--trace", default=None,
+                    help="routing trace JSON (save_trace format); replaces the generated patterns (bench.py:343-346)")
     ap.add_argument("--patterns", nargs="+", default=sorted(GENERATORS))
     ap.add_argument("--seq-lens", nargs="+", type=int, default=list(DEFAULT_SEQ_LENS), help="total tokens")
     ap.add_argument("--topk", type=int, default=8)
@@ -245,9 +259,25 @@ def main(argv=None) -> int:
     ap.add_argument("--dump-plan", default=None, metavar="PATH",
                     help="also write the first cell's device plans as plan_to_json documents (bench.py:399-421)")
     args = ap.parse_args(argv)
-    topo, pl = preset(args.preset)
-    cfg = BenchConfig(topo, pl, tuple(args.patterns), tuple(args.seq_lens), args.topk, args.token_bytes,
-                      balancer=args.balancer, variants=tuple(args.variants), seed=args.seed, repeats=args.repeats)
+    try:
+        if Path(args.topology).exists():
+            topo, pl = load_topology(args.topology)
+        else:
+            topo, pl = preset(args.topology)
+    except (OSError, ValueError, KeyError) as exc:
+        print(f"error: topology {args.topology!r}: {exc}", file=sys.stderr)
+        return 2
+    trace, label, token_bytes, topk = None, "trace", args.token_bytes, args.topk
+    if args.trace:
+        try:
+            trace, token_bytes = load_trace(args.trace)
+        except (OSError, ValueError, KeyError) as exc:
+            print(f"error: trace {args.trace!r}: {exc}", file=sys.stderr)
+            return 2
+        label, topk = Path(args.trace).name, trace.topk
+    cfg = BenchConfig(topo, pl, tuple(args.patterns), tuple(args.seq_lens), topk, token_bytes,
+                      balancer=args.balancer, variants=tuple(args.variants), seed=args.seed, repeats=args.repeats,
+                      trace=trace, trace_label=label)
     if args.dump_plan:
         from .api import run_exchange
         from .wire import plan_to_json

@@ -428,6 +428,28 @@ def test_bench_matrix_rows_on_gpu():
 
 
 @pytest.mark.gpu
+def test_bench_matrix_from_recorded_trace(tmp_path):
+    """A captured routing drives the GPU matrix (--topology FILE --trace FILE)."""
+    import json
+
+    from paper_2512_22036_b200 import matrix as M
+
+    pkg = _pkg()
+    topo, pl = pkg.preset("test")
+    a = pkg.gen_realworld(512, 4, topo, pl, seed=11, zipf_s=1.0)
+    pkg.save_trace(tmp_path / "cap.json", a, 256)
+    pkg.save_topology(tmp_path / "topo.json", topo, pl)
+    out = tmp_path / "rows.json"
+    assert M.main(["--topology", str(tmp_path / "topo.json"), "--trace", str(tmp_path / "cap.json"), "--variants",
+                   "fused", "balancer_off", "--repeats", "1", "--format", "json", "--out", str(out)]) == 0
+    doc = json.loads(out.read_text())
+    M.validate_result(doc)
+    assert [(r["pattern"], r["seq_len"], r["variant"]) for r in doc["rows"]] == [
+        ("cap.json", 512, "fused"), ("cap.json", 512, "balancer_off")]
+    assert doc["rows"][1]["balancer"] == "static"
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("name", golden_names())
 def test_device_plan_json_matches_oracle_plan(name):
     """§8f #4: the --dump-plan document of the device-built plans (layouts,

@@ -117,7 +117,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
         assert s in _lib.SIGNATURES, f"{s} missing a ctypes signature"
-    assert lib.fs_abi_version() == 1
+    assert lib.fs_abi_version() == 2
 
 
 def test_library_validates_before_touching_cuda():
@@ -127,15 +127,18 @@ def test_library_validates_before_touching_cuda():
     from paper_2512_22036_b200 import _lib
 
     n = c_size_t()
-    _lib.call("fs_region_bytes", 8, 256, 14336, 1000, 1, byref(n))
-    # signal block + 2 parity copies of the epoch-tagged count words (u64 P x E)
-    # + 2 of fan_src (int32 per row) + the activation rows + the expert-output rows
+    _lib.call("fs_region_bytes", 8, 256, 8, 14336, 300, 1000, 1, byref(n))
+    # signal block + 2 parity copies of the epoch-tagged count words (u64 P x
+    # (E + 1)) + the dispatch block words (u64 P x ceil(300 / 128)) + the
+    # duplicate lists (int2 P x 300 x (K - 1)) + the activation rows + the
+    # expert-output rows
     a256 = lambda b: (b + 255) // 256 * 256  # noqa: E731
-    assert n.value == 4096 + 2 * a256(8 * 256 * 8) + 2 * a256(1000 * 4) + 2 * a256(1000 * 14336)
-    _lib.call("fs_region_bytes", 8, 256, 14336, 1000, 0, byref(n))
-    assert n.value == 4096 + 2 * a256(8 * 256 * 8) + 2 * a256(1000 * 4) + a256(1000 * 14336)
+    fixed = 4096 + 2 * a256(8 * 257 * 8) + a256(8 * 3 * 8) + a256(8 * 300 * 7 * 8)
+    assert n.value == fixed + 2 * a256(1000 * 14336)
+    _lib.call("fs_region_bytes", 8, 256, 8, 14336, 300, 1000, 0, byref(n))
+    assert n.value == fixed + a256(1000 * 14336)
     with pytest.raises(ValueError):
-        _lib.call("fs_region_bytes", 0, 256, 14336, 1000, 1, byref(n))
+        _lib.call("fs_region_bytes", 0, 256, 8, 14336, 300, 1000, 1, byref(n))
     owner = (np.arange(8) % 2).astype(np.int32)
     peers = (c_void_p * 2)(1, 2)
     h = c_void_p()
@@ -198,6 +201,31 @@ def test_bench_matrix_cells_fingerprint_and_render():
         M.validate_result({**doc, "rows": [{**row, "variant": "nope"}]})
     with pytest.raises(ValueError):
         M.validate_result({**doc, "rows": [{k: v for k, v in row.items() if k != "dedup_ratio"}]})
+
+
+def test_bench_matrix_trace_and_topology_file(tmp_path):
+    """--trace / --topology FILE (reference bench.py:291-298, 343-346,
+    374-383): a recorded routing replaces the generated cells, its label
+    enters the fingerprint; a bad file is an argument error (exit code 2)."""
+    import paper_2512_22036_b200 as pkg
+    from paper_2512_22036_b200 import matrix as M
+
+    topo, pl = pkg.preset("test")
+    a = pkg.gen_realworld(300, 4, topo, pl, seed=3)
+    tr = tmp_path / "captured.json"
+    pkg.save_trace(tr, a, 96)
+    topo_file = tmp_path / "topo.json"
+    pkg.save_topology(topo_file, topo, pl)
+    back, tb = pkg.load_trace(tr)
+    cfg = M.BenchConfig(topo, pl, topk=4, token_bytes=tb, trace=back, trace_label=tr.name)
+    assert M.cells(cfg) == [("captured.json", 300)]
+    assert np.array_equal(M.cell_assignment(cfg, 0, "captured.json", 300).experts, a.experts)
+    assert cfg.fingerprint_doc()["trace"] == "captured.json"
+    assert cfg.fingerprint() != M.BenchConfig(topo, pl, topk=4, token_bytes=tb).fingerprint()
+    assert M.main(["--topology", str(tmp_path / "missing.json")]) == 2
+    bad = tmp_path / "bad.json"
+    bad.write_text("{}")
+    assert M.main(["--topology", str(topo_file), "--trace", str(bad)]) == 2
 
 
 # ---- wire / golden formats (§8f #4) -----------------------------------------

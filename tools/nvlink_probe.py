@@ -32,22 +32,29 @@ def main() -> int:
         print(json.dumps({"error": "needs 2 GPUs"}))
         return 0
     c = [NvlinkCounters(torch.device("cuda", i)) for i in range(2)]
-    out = {"links": [x.links for x in c], "pci": [x.pci for x in c]}
+    out = {"links": [x.links for x in c], "pci": [x.pci for x in c], "mode": [x.mode for x in c],
+           "rejected": [x.errors for x in c]}
     a = torch.empty(n, dtype=torch.uint8, device="cuda:0").fill_(1)
     b = torch.empty(n, dtype=torch.uint8, device="cuda:1")
     torch.cuda.synchronize("cuda:0")
     torch.cuda.synchronize("cuda:1")
-    for raw in (False, True):
-        key = "raw" if raw else "data"
-        before = [x.read(raw) for x in c]
-        b.copy_(a)
+    for rep in range(2):
+        for x in c:
+            x.start()
+        for _ in range(4):
+            b.copy_(a)
         torch.cuda.synchronize("cuda:0")
         torch.cuda.synchronize("cuda:1")
-        after = [x.read(raw) for x in c]
-        out[f"ce_copy_{key}"] = {f"gpu{i}": {"tx": after[i][0] - before[i][0], "rx": after[i][1] - before[i][1]}
-                                 for i in range(2)}
-    out["bytes"] = n
-    out["mode"] = c[0].mode
+        got = [x.stop() for x in c]
+        out[f"ce_copy_x4_{rep}"] = {f"gpu{i}": {"tx": got[i][0], "rx": got[i][1]} for i in range(2)}
+    try:
+        import subprocess
+
+        out["nvidia_smi_nvlink_gt_d"] = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", "0"],
+                                                       capture_output=True, text=True, timeout=30).stdout[-1500:]
+    except Exception as e:  # noqa: BLE001
+        out["nvidia_smi_nvlink_gt_d"] = repr(e)
+    out["bytes_per_copy"] = n
     print(json.dumps(out, indent=1))
     return 0
 
