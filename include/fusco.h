@@ -119,6 +119,10 @@ int fs_sym_free(int device, void* ptr);
 int fs_ipc_handle(int device, void* ptr, uint8_t* handle64_out);
 int fs_ipc_open(int device, const uint8_t* handle64, void** ptr_out);
 int fs_ipc_close(int device, void* ptr);
+/* Map peer_device's memory into device's address space (one process driving
+ * several GPUs, e.g. the phased multi-GPU emulation the NVLink counter
+ * profile uses; production ranks map peers through CUDA IPC instead). */
+int fs_enable_peer_access(int device, int peer_device);
 
 /* ---- handle ------------------------------------------------------------- */
 

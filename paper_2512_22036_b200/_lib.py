@@ -37,6 +37,7 @@ SIGNATURES = {
     "fs_ipc_handle": (c_int, [c_int, c_void_p, c_void_p]),
     "fs_ipc_open": (c_int, [c_int, c_void_p, POINTER(c_void_p)]),
     "fs_ipc_close": (c_int, [c_int, c_void_p]),
+    "fs_enable_peer_access": (c_int, [c_int, c_int]),
     "fs_create": (
         c_int,
         [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_longlong, c_int, c_void_p, c_void_p, c_void_p,

@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(kCombThreads)
     int n = 0;
     for (;; ++n) {
       const int q = n % nstages;
-      if (n >= nstages) mbar_wait(&empty[q], ((n / nstages) & 1) ^ 1);
+      if (n >= nstages) mbar_wait_bounded(&empty[q], ((n / nstages) & 1) ^ 1, a, kSiteCombinePipe);
       if (u >= items) {  // sentinel: consumers stop at this stage
         if (lane == 0) {
           slot_item[q] = -1;
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(kCombThreads)
     const int ct = threadIdx.x - 32;  // 0 .. 32*kCombConsumers-1
     for (int n = 0;; ++n) {
       const int q = n % nstages;
-      mbar_wait(&full[q], (n / nstages) & 1);
+      mbar_wait_bounded(&full[q], (n / nstages) & 1, a, kSiteCombinePipe);
       const long long u = slot_item[q];
       if (u < 0) break;
       const int i = (int)((uint32_t)u / (uint32_t)S), j = (int)((uint32_t)u - (uint32_t)i * (uint32_t)S);

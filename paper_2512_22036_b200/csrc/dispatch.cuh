@@ -79,14 +79,14 @@ __device__ __forceinline__ void warp_copy_row_cg(V* __restrict__ dst, const V* _
 // count: jcum[k] (cumulative fan-out units after the k-th published job),
 // jorder[k] = (q << 16) | b, then one release of (k << 40 | units) on the
 // work word kWorkFanReady.  Every other warp with nothing left to push
-// claims groups of kFanGroup units (one unit = one kSliceWords slice of one
-// duplicate row) and copies primary -> duplicate rows in its own HBM once
+// claims groups of kFanGroup units (one unit = one duplicate row) and
+// copies primary -> duplicate rows in its own HBM once
 // the published prefix covers them — so duplicates of early blocks are
 // fanned out while later blocks are still crossing NVLink.  Replaces the
 // reference's "forwarders fan out after all landings" (engine.py:845-847)
 // and its expected-byte completion counters (engine.py:979-1031).
 // ===========================================================================
-constexpr int kFanGroup = 4;
+constexpr int kFanGroup = 2;  // duplicate rows per fan-out claim
 
 __device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
   unsigned long long v;
@@ -99,7 +99,7 @@ __device__ __forceinline__ void st_release_gpu_u64(unsigned long long* p, unsign
 constexpr unsigned long long kUnitMask = (1ull << 40) - 1;
 
 // The watcher warp: publishes landed jobs until every one is in (or timeout).
-static __device__ void fan_watch(const FsArgs& a, uint32_t epoch, int S) {
+static __device__ void fan_watch(const FsArgs& a, uint32_t epoch) {
   const int P = a.world, s = a.rank, lane = threadIdx.x & 31;
   const int par = (int)(epoch & 1u);
   unsigned long long* ready = work_ctr(a, epoch, kWorkFanReady);
@@ -142,7 +142,7 @@ static __device__ void fan_watch(const FsArgs& a, uint32_t epoch, int S) {
       }
     }
     const bool pub = rdy && nd > 0;
-    const unsigned long long mine = pub ? (unsigned long long)nd * (unsigned long long)S : 0ull;
+    const unsigned long long mine = pub ? (unsigned long long)nd : 0ull;  // fan-out units are whole rows
     // inclusive warp scan of the newly published units
     unsigned long long inc = mine;
 #pragma unroll
@@ -169,7 +169,7 @@ static __device__ void fan_watch(const FsArgs& a, uint32_t epoch, int S) {
       __nanosleep(64);
     }
   }
-  if (timed_out && lane == 0) record_error(a.status, FS_ETIMEOUT);
+  if (timed_out && lane == 0) record_error(a.status, FS_ETIMEOUT, kSiteDispBlocks);
   if (a.trace != nullptr && lane == 0) a.trace[FS_TRACE_DISPATCH_ARRIVED] = globaltimer();
   __syncwarp();
   if (lane == 0) st_release_gpu_u64(done, 1ull);
@@ -181,7 +181,6 @@ __device__ void fan_work(const FsArgs& a, uint32_t epoch, size_t act_off, int nv
   constexpr int U = MoveCfg<V>::U;
   constexpr int SW = 32 * U;
   const int lane = threadIdx.x & 31;
-  const int S = (nv + SW - 1) / SW;
   unsigned long long* ctr = work_ctr(a, epoch, kWorkFanout);
   const unsigned long long* ready = work_ctr(a, epoch, kWorkFanReady);
   const unsigned long long* done = work_ctr(a, epoch, kWorkFanDone);
@@ -200,6 +199,7 @@ __device__ void fan_work(const FsArgs& a, uint32_t epoch, size_t act_off, int nv
       const unsigned long long u = g0 + gi;
       // wait until the published prefix covers u (or every job is in)
       unsigned backoff = 64;
+      unsigned long long tw = 0;
       while (u >= (seen & kUnitMask)) {
         // lane 0 polls (with backoff: thousands of warps may wait here)
         unsigned long long w = 0, d = 0;
@@ -212,6 +212,13 @@ __device__ void fan_work(const FsArgs& a, uint32_t epoch, size_t act_off, int nv
         seen = w;
         if (u < (seen & kUnitMask)) break;
         if (d) return;  // final prefix read after `done`: u is past the last unit
+        // bounded like every wait (the watcher itself gives up after timeout_ns)
+        if (tw == 0) {
+          tw = globaltimer();
+        } else if (globaltimer() - tw > 2 * a.timeout_ns) {
+          if (lane == 0) record_error(a.status, FS_ETIMEOUT, kSiteDispWorker);
+          return;
+        }
         __nanosleep(backoff);
         backoff = backoff < 1024 ? backoff * 2 : 1024;
       }
@@ -228,35 +235,37 @@ __device__ void fan_work(const FsArgs& a, uint32_t epoch, size_t act_off, int nv
         k += 32;
       }
       if (k >= npub) {  // cannot happen (jcum[npub-1] is the published total > u): fail loudly, never spin
-        if (lane == 0) record_error(a.status, FS_ERANGE);
+        if (lane == 0) record_error(a.status, FS_ERANGE, kSiteDispSchedule);
         return;
       }
       const unsigned long long base = k ? __ldcg(a.fan_jcum + k - 1) : 0ull;
       const uint32_t jo = __ldcg(a.fan_jorder + k);
       const int q = (int)(jo >> 16), b = (int)(jo & 0xffffu);
-      const unsigned long long loc = u - base;
-      const int entry = (int)(loc / (unsigned)S), sl = (int)(loc - (unsigned long long)entry * S);
+      const int entry = (int)(u - base);  // the job's entry = one duplicate row
       const int2 rp = __ldcg(dq + (size_t)q * a.dupq_cap + (size_t)b * per_block + entry);
       if (rp.x < 0 || rp.x >= a.max_rows || rp.y < 0 || rp.y >= a.max_rows) {
-        if (lane == 0) record_error(a.status, FS_ERANGE);
+        if (lane == 0) record_error(a.status, FS_ERANGE, kSiteRows);
         continue;
       }
-      const int w0 = sl * SW, rem = nv - w0;
-      const V* src = act + (size_t)rp.y * nv + w0;
-      V* dst = act + (size_t)rp.x * nv + w0;
-      V v[U];
+      // the whole row, slice by slice (one schedule lookup per row)
+      const V* src = act + (size_t)rp.y * nv;
+      V* dst = act + (size_t)rp.x * nv;
+      for (int w0 = 0; w0 < nv; w0 += SW) {
+        const int rem = nv - w0;
+        V v[U];
 #pragma unroll
-      for (int jj = 0; jj < U; ++jj)
-        if (jj * 32 + lane < rem) v[jj] = ld_cg(src + jj * 32 + lane);
+        for (int jj = 0; jj < U; ++jj)
+          if (jj * 32 + lane < rem) v[jj] = ld_cg(src + w0 + jj * 32 + lane);
 #pragma unroll
-      for (int jj = 0; jj < U; ++jj)
-        if (jj * 32 + lane < rem) st_na(dst + jj * 32 + lane, v[jj]);
+        for (int jj = 0; jj < U; ++jj)
+          if (jj * 32 + lane < rem) st_na(dst + w0 + jj * 32 + lane, v[jj]);
+      }
     }
   }
 }
 
 template <typename V>
-__global__ void __launch_bounds__(kMoveThreads)
+__global__ void __launch_bounds__(kMoveThreads, 3)
     dispatch_kernel(FsArgs a, const V* __restrict__ x, const void* __restrict__ idx,
                     const int32_t* __restrict__ row_of, int phase) {
   TraceLast trace_last_(a, FS_TRACE_DISPATCH_LAST);
@@ -282,8 +291,11 @@ __global__ void __launch_bounds__(kMoveThreads)
 
   if (pusher) {
     // A claim is one (token, slice) unit, or a whole token (all S slices)
-    // with a.claim_tokens: fewer claims and one completion count per token,
-    // at the price of a coarser dynamic balance.
+    // with a.claim_tokens.  The loop keeps three things in flight across
+    // iterations so no round trip sits on the critical path: the claim after
+    // next (lane 0's atomic, read one iteration later), the next claim's
+    // (expert, row) metadata, and the previous claim's block count (its
+    // completion check runs after this unit's payload loads are issued).
     const uint32_t uS = (uint32_t)S;
     const uint32_t G = a.claim_tokens ? uS : 1u;  // units per claim
     const long long claims = a.claim_tokens ? (long long)T : (long long)T * S;
@@ -297,14 +309,30 @@ __global__ void __launch_bounds__(kMoveThreads)
     const long long pnum = (long long)gridDim.x * npw - (wexcl ? 1 : 0);
     auto token_of = [&](long long c) { return (int)(G == uS ? (uint32_t)c : (uint32_t)c / uS); };
     long long c = dyn ? claim_warp(ctr) : pidx;
-    KMeta nxt = c < claims ? load_meta(a, idx, row_of, token_of(c), lane) : KMeta{0, -1};
+    KMeta cur = c < claims ? load_meta(a, idx, row_of, token_of(c), lane) : KMeta{0, -1};
+    long long cn = dyn ? claim_warp(ctr) : c + pnum;
+    KMeta nxt = cn < claims ? load_meta(a, idx, row_of, token_of(cn), lane) : KMeta{0, -1};
+    // lane 0's deferred block count of the previous claim
+    int pend_b = -1;
+    uint32_t pend_prev = 0, pend_total = 0;
     while (c < claims) {
       const int i = token_of(c);
       const int sl0 = G == uS ? 0 : (int)((uint32_t)c - (uint32_t)i * uS);
-      const KMeta cur = nxt;
-      const long long cn = dyn ? claim_warp(ctr) : c + pnum;  // next claim: taken and prefetched now
-      if (cn < claims) nxt = load_meta(a, idx, row_of, token_of(cn), lane);
-      // destinations of the token (lane k < K: owner and row of its k-th expert)
+      // 1. payload loads of the first slice: independent of everything else
+      V v[U];
+      {
+        const int w0 = sl0 * SW, rem = nv - w0;
+        const V* src = x + (size_t)i * nv + w0;
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (j * 32 + lane < rem) v[j] = ld_nc(src + j * 32 + lane);
+      }
+      // 2. the claim after next, in flight while this unit is processed
+      unsigned long long raw = 0;
+      if (dyn && lane == 0) raw = atomicAdd(ctr, 1ull);
+      // 3. the previous claim completed its block?
+      if (P > 1 && lane == 0 && pend_b >= 0 && pend_prev == pend_total) block_complete(a, epoch, pend_b);
+      // 4. destinations of the token (lane k < K: owner and row of its k-th expert)
       int g = -1 - lane, r = -1;  // lanes >= K get unique negative keys
       if (lane < K) {
         g = owner_sm[cur.e];
@@ -324,16 +352,14 @@ __global__ void __launch_bounds__(kMoveThreads)
       // rank spread their first stores over different peers.
       const int rot = dyn ? (i + s) % K : 0;
       const uint32_t mrot = (dmask >> rot) | (rot ? (dmask << (32 - rot)) : 0u);
+      // 5. stores, slice by slice
       for (int sl = sl0; sl < sl0 + (int)G; ++sl) {
-        // payload loads first: they do not depend on the destinations
-        const int w0 = sl * SW;
-        const V* src = x + (size_t)i * nv + w0;
-        const int rem = nv - w0;
-        V v[U];
+        const int w0 = sl * SW, rem = nv - w0;
+        if (sl != sl0) {
+          const V* src = x + (size_t)i * nv + w0;
 #pragma unroll
-        for (int j = 0; j < U; ++j) {
-          const int w = j * 32 + lane;
-          if (w < rem) v[j] = ld_nc(src + w);
+          for (int j = 0; j < U; ++j)
+            if (j * 32 + lane < rem) v[j] = ld_nc(src + j * 32 + lane);
         }
         uint32_t m = mrot;
         while (m) {
@@ -344,26 +370,32 @@ __global__ void __launch_bounds__(kMoveThreads)
           const int rd = __shfl_sync(kFull, r, d);
           V* dst = reinterpret_cast<V*>(a.peer[gd] + act_off) + (size_t)rd * nv + w0;
 #pragma unroll
-          for (int j = 0; j < U; ++j) {
-            const int w = j * 32 + lane;
-            if (w < rem) st_na(dst + w, v[j]);
-          }
+          for (int j = 0; j < U; ++j)
+            if (j * 32 + lane < rem) st_na(dst + j * 32 + lane, v[j]);
         }
       }
-      if (P > 1) {  // completion accounting of the claim's block
+      // 6. count the claim into its block (checked next iteration)
+      if (P > 1) {
         __syncwarp();
         if (lane == 0) {
           const int nt = min(kBlockTokens, T - b * kBlockTokens);
-          block_units_done(a, epoch, b, G, (uint32_t)(nt * S));
+          pend_prev = block_count(a, epoch, b, G) + G;
+          pend_total = (uint32_t)(nt * S);
+          pend_b = b;
         }
       }
+      // 7. rotate the pipeline
       c = cn;
+      cur = nxt;
+      cn = dyn ? (long long)__shfl_sync(kFull, raw, 0) : cn + pnum;
+      if (cn < claims) nxt = load_meta(a, idx, row_of, token_of(cn), lane);
     }
+    if (P > 1 && lane == 0 && pend_b >= 0 && pend_prev == pend_total) block_complete(a, epoch, pend_b);
   }
   griddep_launch_dependents();  // the combine may start its prologue
   trace_stamp(a, FS_TRACE_DISPATCH_PUSHED);
   if (remote) {
-    if (watcher) fan_watch(a, epoch, S);
+    if (watcher) fan_watch(a, epoch);
     fan_work<V>(a, epoch, act_off, nv, kWarps);
   }
   trace_stamp(a, FS_TRACE_DISPATCH_END);
@@ -431,7 +463,7 @@ __global__ void __launch_bounds__(kTmaThreads)
         for (int i = blockIdx.x; i < T; i += gridDim.x, ++n) {
           if (n < nslots) continue;
           const int q = n % nslots;
-          mbar_wait(&empty[q], ((n / nslots) & 1) ^ 1);
+          mbar_wait_bounded(&empty[q], ((n / nslots) & 1) ^ 1, a, kSiteDispatchPipe);
           mbar_arrive_expect_tx(&full[q], (uint32_t)tb);
           bulk_load(ring + (size_t)q * slot_bytes, x + (size_t)i * tb, (uint32_t)tb, &full[q]);
         }
@@ -454,7 +486,7 @@ __global__ void __launch_bounds__(kTmaThreads)
         const bool direct = lane < K && r >= 0 && (a.nodedup || first_lane == lane || g == s);
         if (P > 1 && lane < K && r >= 0 && !direct && r_first >= 0)
           list_duplicate(a, epoch, g, i / kBlockTokens, r, r_first);
-        mbar_wait(&full[q], (n / nslots) & 1);
+        mbar_wait_bounded(&full[q], (n / nslots) & 1, a, kSiteDispatchPipe);
         // each destination lane issues its own bulk store (per-thread bulk
         // groups); every lane commits one group per token so the lag below
         // counts tokens on all lanes
@@ -496,8 +528,7 @@ __global__ void __launch_bounds__(kTmaThreads)
 
   trace_stamp(a, FS_TRACE_DISPATCH_PUSHED);
   if (remote) {  // watcher: CTA 0's warp 3; every warp fans out once it has no push work
-    if (blockIdx.x == 0 && warp == 3) fan_watch(a, epoch, (tb / 16 + MoveCfg<int4>::kSliceWords - 1) /
-                                                              MoveCfg<int4>::kSliceWords);
+    if (blockIdx.x == 0 && warp == 3) fan_watch(a, epoch);
     fan_work<int4>(a, epoch, act_off, tb / 16, kTmaThreads / 32);
   }
   trace_stamp(a, FS_TRACE_DISPATCH_END);

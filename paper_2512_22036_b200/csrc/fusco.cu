@@ -102,6 +102,7 @@ struct fs_ctx {
   uint32_t* jorder_d;              // [P * nbmax]
   int push_warps;                  // warps per dispatch CTA that push before fanning out
   int claim_tokens;                // dispatch claim granularity: 1 = whole tokens, 0 = (token, slice) units
+  int dbg_relaxed;                 // FUSCO_DBG_BLK=1: unordered block counts (timing experiments only)
   int disp_ctas_per_sm;            // P > 1 warp-mover grid cap (0 = occupancy)
   unsigned long long* trace_d;  // FS_NTRACE stamps when FUSCO_TRACE=1, else null
 };
@@ -138,6 +139,7 @@ FsArgs make_args(const fs_ctx* h, int T, int idx64) {
   a.dupq_cap = h->L.dupq_cap;
   a.push_warps = h->push_warps;
   a.claim_tokens = h->claim_tokens;
+  a.dbg_relaxed = h->dbg_relaxed;
   a.blkdone = h->blkdone_d;
   a.dupcnt = h->dupcnt_d;
   a.fan_jcum = h->jcum_d;
@@ -246,6 +248,21 @@ int fs_ipc_open(int device, const uint8_t* handle64, void** ptr_out) {
   void* p = nullptr;
   FS_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
   *ptr_out = p;
+  return FS_OK;
+}
+
+int fs_enable_peer_access(int device, int peer_device) {
+  if (device == peer_device) return FS_OK;
+  FS_CUDA(cudaSetDevice(device));
+  int can = 0;
+  FS_CUDA(cudaDeviceCanAccessPeer(&can, device, peer_device));
+  if (!can) return fail(FS_EINVAL, "fs_enable_peer_access: no peer access between these devices");
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return FS_OK;
+  }
+  FS_CUDA(e);
   return FS_OK;
 }
 
@@ -381,6 +398,8 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
     h->push_warps = pw ? std::max(1, std::min(kMoveThreads / 32, atoi(pw))) : kMoveThreads / 32;
     const char* cl = getenv("FUSCO_CLAIM");  // unit | token
     h->claim_tokens = cl && std::string(cl) == "token";
+    const char* db = getenv("FUSCO_DBG_BLK");
+    h->dbg_relaxed = db && std::string(db) == "1";
     const char* dc = getenv("FUSCO_DISP_CTAS");  // P > 1 warp mover: CTAs per SM cap
     h->disp_ctas_per_sm = dc ? std::max(1, std::min(kMaxCtasPerSm, atoi(dc))) : 0;
     const char* nd = getenv("FUSCO_NODEDUP");
@@ -444,7 +463,7 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
       (e = dalloc((void**)&h->chunk_cnt_d, (size_t)max_chunks * num_experts * 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->totals_d, (size_t)2 * num_experts * 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->stat_part_d, (size_t)2 * 8 * 8)) != cudaSuccess ||
-      (e = dalloc((void**)&h->status_d, 4)) != cudaSuccess ||
+      (e = dalloc((void**)&h->status_d, 8)) != cudaSuccess ||
       (e = dalloc((void**)&h->num_rows_d, 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->epoch_d, 4)) != cudaSuccess ||
       (e = dalloc((void**)&h->work_d, kWorkWords * 8)) != cudaSuccess ||
@@ -457,7 +476,7 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
       (e = cudaMemcpy(h->node_of_d, nodes.data(), world * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(h->perm_d, perm.data(), num_experts * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(h->seg_d, seg.data(), (world + 1) * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
-      (e = cudaMemset(h->status_d, 0, 4)) != cudaSuccess ||
+      (e = cudaMemset(h->status_d, 0, 8)) != cudaSuccess ||
       (e = cudaMemset(h->num_rows_d, 0, 4)) != cudaSuccess ||
       (e = cudaMemset(h->epoch_d, 0, 4)) != cudaSuccess ||
       (e = cudaMemset(h->work_d, 0, kWorkWords * 8)) != cudaSuccess ||
@@ -728,11 +747,23 @@ int fs_check(fs_handle_t h, void* stream) {
   if (!h) return fail(FS_EINVAL, "null handle");
   FS_CUDA(cudaSetDevice(h->device));
   FS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
-  int status = 0;
-  FS_CUDA(cudaMemcpy(&status, h->status_d, 4, cudaMemcpyDeviceToHost));
-  FS_CUDA(cudaMemset(h->status_d, 0, 4));
-  if (status == FS_ETIMEOUT) return fail(FS_ETIMEOUT, "a peer flag wait timed out");
-  if (status == FS_ERANGE) return fail(FS_ERANGE, "routing out of range (expert id or row capacity)");
+  int st[2] = {0, 0};
+  FS_CUDA(cudaMemcpy(st, h->status_d, 8, cudaMemcpyDeviceToHost));
+  FS_CUDA(cudaMemset(h->status_d, 0, 8));
+  const int status = st[0];
+  static const char* kSites[] = {"",
+                                 " (planner: peer count words)",
+                                 " (dispatch: a source's token count)",
+                                 " (dispatch: a source's block words)",
+                                 " (dispatch fan-out worker: published schedule)",
+                                 " (dispatch fan-out worker: inconsistent schedule)",
+                                 " (combine: a peer's outputs-ready flag)",
+                                 " (combine: TMA stage pipeline)",
+                                 " (dispatch: TMA slot pipeline)",
+                                 " (row index outside the activation buffer)"};
+  const std::string where = (st[1] > 0 && st[1] < (int)(sizeof(kSites) / sizeof(kSites[0]))) ? kSites[st[1]] : "";
+  if (status == FS_ETIMEOUT) return fail(FS_ETIMEOUT, "a peer flag wait timed out" + where);
+  if (status == FS_ERANGE) return fail(FS_ERANGE, "routing out of range (expert id or row capacity)" + where);
   if (status == FS_EINVAL) return fail(FS_EINVAL, "a token routes to the same expert twice");
   if (status != FS_OK) return fail(status, "device reported an error");
   return FS_OK;

@@ -57,10 +57,11 @@ struct FsArgs {
   long long dupq_cap;        // duplicate-list entries per source in a region (max_tokens * (K - 1))
   int push_warps;            // warps per CTA that push first (the rest fan out from the start)
   int claim_tokens;          // 1: pushers claim whole tokens (all slices), 0: (token, slice) units
+  int dbg_relaxed;           // timing experiments only: block counts without release ordering
   int32_t* chunk_cnt;        // [chunks][E] scratch (per handle)
   int32_t* totals;           // [2][E] per-parity per-expert atomic totals (per handle)
   long long* stat_part;      // [2][8] per-parity atomic statistics accumulators
-  int* status;               // first error code, FS_OK when clean
+  int* status;               // [2]: first error code (FS_OK when clean), ErrSite of a timeout
   int* num_rows;             // rows of the own activation buffer this epoch
   unsigned long long timeout_ns;
   unsigned long long* trace;  // optional globaltimer stamps (FUSCO_TRACE=1), see FS_TRACE_*
@@ -110,8 +111,21 @@ struct TraceLast {
   }
 };
 
-__device__ __forceinline__ void record_error(int* status, int code) {
-  atomicCAS(status, FS_OK, code);
+// Where a kernel gave up (status word 1, read back by fs_check with the code).
+enum ErrSite : int {
+  kSiteNone = 0,
+  kSiteLayoutCounts = 1,     // planner: a peer's count words of this epoch
+  kSiteDispTokens = 2,       // dispatch watcher: a source's token count word
+  kSiteDispBlocks = 3,       // dispatch watcher: a source's block words
+  kSiteDispWorker = 4,       // dispatch fan-out worker: the published schedule
+  kSiteDispSchedule = 5,     // dispatch fan-out worker: inconsistent schedule
+  kSiteCombineReady = 6,     // combine: a peer's "outputs ready" flag
+  kSiteCombinePipe = 7,      // combine TMA engine: shared-memory stage pipeline
+  kSiteDispatchPipe = 8,     // dispatch TMA engine: shared-memory slot pipeline
+  kSiteRows = 9,             // a row index outside the activation buffer
+};
+__device__ __forceinline__ void record_error(int* status, int code, int site = kSiteNone) {
+  if (atomicCAS(status, FS_OK, code) == FS_OK) status[1] = site;
 }
 
 __device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
@@ -146,11 +160,12 @@ __device__ __forceinline__ void red_release_sys_add_u64(unsigned long long* p, u
 }
 
 // Spin until *p >= target (wrap-safe for u32 epochs); false on timeout.
-__device__ __forceinline__ bool wait_u32_geq(const uint32_t* p, uint32_t target, const FsArgs& a) {
+__device__ __forceinline__ bool wait_u32_geq(const uint32_t* p, uint32_t target, const FsArgs& a,
+                                             int site = kSiteCombineReady) {
   const unsigned long long t0 = globaltimer();
   while ((int32_t)(ld_acquire_sys_u32(p) - target) < 0) {
     if (globaltimer() - t0 > a.timeout_ns) {
-      record_error(a.status, FS_ETIMEOUT);
+      record_error(a.status, FS_ETIMEOUT, site);
       return false;
     }
   }
@@ -192,7 +207,7 @@ __device__ __forceinline__ int read_count_word(const FsArgs& a, int parity, uint
     const unsigned long long t0 = globaltimer();
     do {
       if (globaltimer() - t0 > a.timeout_ns) {
-        record_error(a.status, FS_ETIMEOUT);
+        record_error(a.status, FS_ETIMEOUT, kSiteDispTokens);
         return 0;
       }
       w = ld_acquire_sys_u64(p);
@@ -214,7 +229,7 @@ __device__ __forceinline__ void gather_counts(const FsArgs& a, int parity, uint3
       const unsigned long long t0 = globaltimer();
       do {
         if (globaltimer() - t0 > a.timeout_ns) {
-          record_error(a.status, FS_ETIMEOUT);
+          record_error(a.status, FS_ETIMEOUT, kSiteLayoutCounts);
           break;
         }
         w = ld_acquire_sys_u64(p);
@@ -255,17 +270,27 @@ __device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsign
 __device__ __forceinline__ unsigned long long* blkflag_ptr(const FsArgs& a, int g, int src, int b) {
   return reinterpret_cast<unsigned long long*>(a.peer[g] + a.off_blkflag) + (size_t)src * a.nbmax + b;
 }
-__device__ __forceinline__ void block_units_done(const FsArgs& a, uint32_t epoch, int b, uint32_t n,
-                                                 uint32_t total) {
+// Count n units of block b; returns the previous count (the caller that
+// brings it to the block's total completes the block).
+__device__ __forceinline__ uint32_t block_count(const FsArgs& a, uint32_t epoch, int b, uint32_t n) {
+  uint32_t* ctr = a.blkdone + ((size_t)(epoch & 1u) * a.nbmax + b) * kBlkStride;
+  // a.dbg_relaxed (FUSCO_DBG_BLK=1, timing experiments only): relaxed count, no ordering
+  return a.dbg_relaxed ? atomicAdd(ctr, n) : atom_add_acq_rel_gpu_u32(ctr, n);
+}
+// Every unit of block b is counted (and acquired): release the block word on
+// every destination with its duplicate-list length.
+__device__ __forceinline__ void block_complete(const FsArgs& a, uint32_t epoch, int b) {
   const int par = (int)(epoch & 1u);
-  const uint32_t prev = atom_add_acq_rel_gpu_u32(a.blkdone + ((size_t)par * a.nbmax + b) * kBlkStride, n);
-  if (prev + n != total) return;
   __threadfence_system();
   for (int g = 0; g < a.world; ++g) {
     if (g == a.rank) continue;
     const uint32_t nd = ld_relaxed_gpu_u32(a.dupcnt + ((size_t)par * a.world + g) * a.nbmax + b);
     st_release_sys_u64(blkflag_ptr(a, g, a.rank, b), ((unsigned long long)epoch << 32) | nd);
   }
+}
+__device__ __forceinline__ void block_units_done(const FsArgs& a, uint32_t epoch, int b, uint32_t n,
+                                                 uint32_t total) {
+  if (block_count(a, epoch, b, n) + n == total) block_complete(a, epoch, b);
 }
 // Duplicate-list entry of (dup row, primary row) on rank g for block b.
 __device__ __forceinline__ void list_duplicate(const FsArgs& a, uint32_t epoch, int g, int b, int row, int prim) {
@@ -379,6 +404,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// The engines' pipeline waits: bounded like every flag wait, so a lost
+// transaction surfaces as FS_ETIMEOUT through fs_check instead of a hang.
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity, const FsArgs& a, int site) {
+  if (mbar_try_wait(bar, parity)) return;
+  const unsigned long long t0 = globaltimer();
+  while (!mbar_try_wait(bar, parity)) {
+    if (globaltimer() - t0 > a.timeout_ns) {
+      record_error(a.status, FS_ETIMEOUT, site);
+      return;
+    }
+  }
 }
 // global -> shared (this CTA), completion counted on an mbarrier
 __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {

@@ -197,6 +197,10 @@ class Rank:
         """The symmetric expert-output rows (same row layout as act)."""
         return self._rows_view(1, rows, dtype)
 
+    def _stream(self, stream):
+        """The given stream, else the current stream of this rank's device."""
+        return stream_ptr(stream if stream is not None else torch.cuda.current_stream(self.device))
+
     # -- hot path -----------------------------------------------------------
     def new_plan(self, topk_idx: torch.Tensor, with_masks: bool = True) -> Plan:
         T = topk_idx.shape[0]
@@ -231,7 +235,7 @@ class Rank:
         call(
             "fs_layout", self.handle, ptr(plan.topk_idx), ib, plan.num_tokens, ptr(plan.row_of),
             ptr(plan.expert_counts), ptr(plan.expert_offsets), ptr(plan.first_mask),
-            ptr(plan.rank_mask), ptr(plan.stats), phase, stream_ptr(stream),
+            ptr(plan.rank_mask), ptr(plan.stats), phase, self._stream(stream),
         )
         plan.epoch = self.epoch
         return plan
@@ -245,7 +249,7 @@ class Rank:
             raise ValueError("plan is stale: build a new plan (fs_layout) before dispatch")
         call(
             "fs_dispatch", self.handle, ptr(x), ptr(plan.topk_idx), plan.topk_idx.element_size(),
-            ptr(plan.row_of), plan.num_tokens, phase, stream_ptr(stream),
+            ptr(plan.row_of), plan.num_tokens, phase, self._stream(stream),
         )
 
     def combine(
@@ -276,12 +280,12 @@ class Rank:
         call(
             "fs_combine", self.handle, ptr(plan.topk_idx), plan.topk_idx.element_size(), ptr(plan.row_of),
             ptr(topk_w), topk_w.element_size(), plan.num_tokens, ptr(out), dtype_code, src, acc, phase,
-            stream_ptr(stream),
+            self._stream(stream),
         )
 
     def check(self, stream=None) -> None:
         """Synchronise and raise if a kernel recorded an error (timeout, range)."""
-        call("fs_check", self.handle, stream_ptr(stream))
+        call("fs_check", self.handle, self._stream(stream))
 
 
 def region_bytes(world: int, num_experts: int, topk: int, token_bytes: int, max_tokens: int, max_rows: int,
@@ -301,7 +305,13 @@ def default_max_rows(world: int, max_tokens: int, topk: int, owner: np.ndarray) 
 
 
 class EmulatedCluster:
-    """P ranks on the current GPU (see module docstring)."""
+    """P ranks on the current GPU (see module docstring).
+
+    ``devices=[d0, d1, ...]`` instead places rank r's region and kernels on
+    GPU d_r (one process, peer access enabled between them): the same phased
+    launches then move real bytes over NVLink with no kernel waiting on
+    another rank's, so a single-process profiler can count each kernel's
+    NVLink traffic (tools/ncu_nvlink.py)."""
 
     def __init__(
         self,
@@ -319,10 +329,20 @@ class EmulatedCluster:
         timeout_ms: int = 0,
         nodedup: bool = False,
         balance: bool = True,
+        devices=None,
     ):
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         if self.device.index is None:
             self.device = torch.device("cuda", torch.cuda.current_device())
+        if devices is not None:
+            if len(devices) != world:
+                raise ValueError("devices must list one GPU per rank")
+            self.devices = [torch.device("cuda", torch.device(d).index if not isinstance(d, int) else d)
+                            for d in devices]
+            self.device = self.devices[0]
+        else:
+            self.devices = [self.device] * world
+        self.multi_device = len({d.index for d in self.devices}) > 1
         owner = np.arange(num_experts) % world if owner is None else np.asarray(owner)
         self.world = world
         self.token_bytes = token_bytes
@@ -331,13 +351,19 @@ class EmulatedCluster:
         mr = max_rows or default_max_rows(world, max_tokens, topk, owner)
         nbytes = region_bytes(world, num_experts, topk, token_bytes, max_tokens, mr, with_act_out)
         self.regions: list[int] = []
-        for _ in range(world):
+        for r in range(world):
             p = c_void_p()
-            call("fs_sym_alloc", self.device.index, nbytes, byref(p))
+            call("fs_sym_alloc", self.devices[r].index, nbytes, byref(p))
             self.regions.append(p.value)
+        if self.multi_device:
+            idx = sorted({d.index for d in self.devices})
+            for a in idx:
+                for b in idx:
+                    if a != b:
+                        call("fs_enable_peer_access", a, b)
         self.ranks = [
             Rank(
-                device=self.device, rank=r, world=world, num_experts=num_experts, topk=topk,
+                device=self.devices[r], rank=r, world=world, num_experts=num_experts, topk=topk,
                 token_bytes=token_bytes, max_tokens=max_tokens, owner=owner, node_of=node_of,
                 regions=self.regions, max_rows=mr, with_act_out=with_act_out, grid_ctas=grid_ctas,
                 timeout_ms=timeout_ms, nodedup=nodedup, balance=balance,
@@ -348,8 +374,8 @@ class EmulatedCluster:
     def close(self) -> None:
         for r in getattr(self, "ranks", []):
             r.close()
-        for p in getattr(self, "regions", []):
-            _lib.load().fs_sym_free(self.device.index, c_void_p(p))
+        for d, p in zip(getattr(self, "devices", []), getattr(self, "regions", [])):
+            _lib.load().fs_sym_free(d.index, c_void_p(p))
         self.ranks, self.regions = [], []
 
     def __enter__(self):
@@ -373,22 +399,32 @@ class EmulatedCluster:
     def layout(self, topk_idx: list[torch.Tensor], with_masks: bool = True) -> list[Plan]:
         return self.layout_into([r.new_plan(t, with_masks) for r, t in zip(self.ranks, topk_idx)])
 
+    def _phase_done(self) -> None:
+        """Across GPUs, a phase of every rank completes before the next starts
+        (on one GPU the stream order already guarantees it)."""
+        if self.multi_device:
+            for d in sorted({d.index for d in self.devices}):
+                torch.cuda.synchronize(d)
+
     def layout_into(self, plans: list[Plan]) -> list[Plan]:
         """Re-plan into existing Plan tensors (same routing tensors; e.g. a graph-captured step)."""
         for ph in self._phases():
             for r, p in zip(self.ranks, plans):
                 r.layout(p, ph)
+            self._phase_done()
         return plans
 
     def dispatch(self, xs: list[torch.Tensor], plans: list[Plan]) -> None:
         for ph in self._phases():
             for r, x, p in zip(self.ranks, xs, plans):
                 r.dispatch(x, p, ph)
+            self._phase_done()
 
     def combine(self, plans, ws, outs, *, dtype_code: int, src: int = FS_SRC_ACT, acc: int = FS_ACC_F32):
         for ph in self._phases():
             for r, p, w, o in zip(self.ranks, plans, ws, outs):
                 r.combine(p, w, o, dtype_code=dtype_code, src=src, acc=acc, phase=ph)
+            self._phase_done()
 
     def check(self) -> None:
         for r in self.ranks:
