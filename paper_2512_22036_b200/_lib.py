@@ -88,7 +88,8 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path is not None else LIB_PATH
+    # FUSCO_LIB: an alternative build of the same ABI (compile-time experiments)
+    p = Path(path) if path is not None else Path(os.environ.get("FUSCO_LIB", LIB_PATH))
     if not p.exists():
         raise FuscoError(
             FS_ECUDA,

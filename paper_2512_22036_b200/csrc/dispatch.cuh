@@ -88,6 +88,25 @@ __device__ __forceinline__ void warp_copy_row_cg(V* __restrict__ dst, const V* _
 // ===========================================================================
 constexpr int kFanGroup = 2;  // duplicate rows per fan-out claim
 
+// Per-CTA cache of the published fan-out words (a.fan_poll).
+struct FanPoll {
+  unsigned long long seen, done;
+  int lock;
+};
+__device__ __forceinline__ volatile FanPoll* fan_poll_sm() {
+  __shared__ FanPoll fp;
+  return &fp;
+}
+__device__ __forceinline__ void fan_poll_init() {
+  if (threadIdx.x == 0) {
+    volatile FanPoll* fp = fan_poll_sm();
+    fp->seen = 0;
+    fp->done = 0;
+    fp->lock = 0;
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -201,11 +220,29 @@ __device__ void fan_work(const FsArgs& a, uint32_t epoch, size_t act_off, int nv
       unsigned backoff = 64;
       unsigned long long tw = 0;
       while (u >= (seen & kUnitMask)) {
-        // lane 0 polls (with backoff: thousands of warps may wait here)
+        // lane 0 polls (with backoff: thousands of warps may wait here).
+        // a.fan_poll: one warp per CTA at a time reads the global words and
+        // caches them in shared memory; the CTA's other waiting warps read
+        // the cache (one L2 poller per CTA instead of one per warp)
         unsigned long long w = 0, d = 0;
         if (lane == 0) {
-          d = ld_acquire_gpu_u64(done);
-          w = ld_acquire_gpu_u64(ready);
+          if (a.fan_poll) {
+            volatile FanPoll* fp = fan_poll_sm();
+            w = fp->seen;
+            d = fp->done;
+            if (u >= (w & kUnitMask) && !d && atomicCAS(const_cast<int*>(&fp->lock), 0, 1) == 0) {
+              d = ld_acquire_gpu_u64(done);
+              w = ld_acquire_gpu_u64(ready);
+              if (w > fp->seen) fp->seen = w;
+              fp->done = d;
+              __threadfence_block();
+              atomicExch(const_cast<int*>(&fp->lock), 0);
+            }
+            __threadfence_block();
+          } else {
+            d = ld_acquire_gpu_u64(done);
+            w = ld_acquire_gpu_u64(ready);
+          }
         }
         w = __shfl_sync(kFull, w, 0);
         d = __shfl_sync(kFull, d, 0);
@@ -264,8 +301,11 @@ __device__ void fan_work(const FsArgs& a, uint32_t epoch, size_t act_off, int nv
   }
 }
 
+#ifndef FUSCO_DISP_MINB
+#define FUSCO_DISP_MINB 3  // CTAs per SM the register budget is cut for
+#endif
 template <typename V>
-__global__ void __launch_bounds__(kMoveThreads, 3)
+__global__ void __launch_bounds__(kMoveThreads, FUSCO_DISP_MINB)
     dispatch_kernel(FsArgs a, const V* __restrict__ x, const void* __restrict__ idx,
                     const int32_t* __restrict__ row_of, int phase) {
   TraceLast trace_last_(a, FS_TRACE_DISPATCH_LAST);
@@ -283,6 +323,7 @@ __global__ void __launch_bounds__(kMoveThreads, 3)
   const bool watcher = remote && blockIdx.x == 0 && wcta == kWarps - 1;
   const bool pusher = (phase & FS_PHASE_LOCAL) && !watcher && (!remote || wcta < a.push_warps);
   __shared__ int32_t owner_sm[kMaxExperts];
+  if (phase & FS_PHASE_REMOTE) fan_poll_init();
   if (phase & FS_PHASE_LOCAL) load_owner_table(a, owner_sm);  // static table: before the PDL wait
   griddep_wait();  // row_of / the epoch come from the planner
   const uint32_t epoch = load_epoch(a);
@@ -423,18 +464,24 @@ __host__ __device__ inline int tma_slot_bytes(int tb) { return (tb + 127) & ~127
 template <int LAG>
 __global__ void __launch_bounds__(kTmaThreads)
     dispatch_tma_kernel(FsArgs a, const char* __restrict__ x, const void* __restrict__ idx,
-                        const int32_t* __restrict__ row_of, int phase, int nslots) {
+                        const int32_t* __restrict__ row_of, int phase, int nslots, int ns, int sb) {
   TraceLast trace_last_(a, FS_TRACE_DISPATCH_LAST);
   extern __shared__ __align__(128) char tsm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
   uint64_t* empty = full + kTmaMaxSlots;
   char* ring = tsm + 2 * kTmaMaxSlots * sizeof(uint64_t);
   const int K = a.K, T = a.T, P = a.world, s = a.rank, tb = a.tb;
-  const int slot_bytes = tma_slot_bytes(tb);
+  const int slot_bytes = tma_slot_bytes(sb);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // work unit = (token, column slice of sb bytes; the last one shorter):
+  // ns slices per token keep the units per CTA high enough that the tail of
+  // the strided assignment is a small fraction of the launch
+  const uint32_t uns = (uint32_t)ns;
+  const int units = T * ns;
+  auto unit_bytes = [&](int sl) { return (uint32_t)min(sb, tb - sl * sb); };
   __shared__ int32_t owner_tma[kMaxExperts];
   // Prologue independent of the planner (launched with PDL behind it): barrier
-  // init, expert table, and the first ring-full of token rows streaming in.
+  // init, expert table, and the first ring-full of token slices streaming in.
   if ((phase & FS_PHASE_LOCAL) && threadIdx.x == 0) {
     for (int q = 0; q < nslots; ++q) {
       mbar_init(&full[q], 1);
@@ -442,12 +489,15 @@ __global__ void __launch_bounds__(kTmaThreads)
     }
     mbar_fence_init();
   }
+  if (phase & FS_PHASE_REMOTE) fan_poll_init();
   if (phase & FS_PHASE_LOCAL) load_owner_table(a, owner_tma);
   if ((phase & FS_PHASE_LOCAL) && threadIdx.x == 0) {
     int n = 0;
-    for (int i = blockIdx.x; i < T && n < nslots; i += gridDim.x, ++n) {
-      mbar_arrive_expect_tx(&full[n], (uint32_t)tb);
-      bulk_load(ring + (size_t)n * slot_bytes, x + (size_t)i * tb, (uint32_t)tb, &full[n]);
+    for (int u = blockIdx.x; u < units && n < nslots; u += gridDim.x, ++n) {
+      const int i = (int)((uint32_t)u / uns), sl = u - i * ns;
+      const uint32_t nb = unit_bytes(sl);
+      mbar_arrive_expect_tx(&full[n], nb);
+      bulk_load(ring + (size_t)n * slot_bytes, x + (size_t)i * tb + (size_t)sl * sb, nb, &full[n]);
     }
   }
   griddep_wait();  // row_of / the epoch come from the planner
@@ -458,23 +508,27 @@ __global__ void __launch_bounds__(kTmaThreads)
 
   if ((phase & FS_PHASE_LOCAL) && warp < 2) {
     if (warp == 0) {
-      if (lane == 0) {  // producer (the first nslots rows were issued in the prologue)
+      if (lane == 0) {  // producer (the first nslots units were issued in the prologue)
         int n = 0;
-        for (int i = blockIdx.x; i < T; i += gridDim.x, ++n) {
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++n) {
           if (n < nslots) continue;
           const int q = n % nslots;
+          const int i = (int)((uint32_t)u / uns), sl = u - i * ns;
+          const uint32_t nb = unit_bytes(sl);
           mbar_wait_bounded(&empty[q], ((n / nslots) & 1) ^ 1, a, kSiteDispatchPipe);
-          mbar_arrive_expect_tx(&full[q], (uint32_t)tb);
-          bulk_load(ring + (size_t)q * slot_bytes, x + (size_t)i * tb, (uint32_t)tb, &full[q]);
+          mbar_arrive_expect_tx(&full[q], nb);
+          bulk_load(ring + (size_t)q * slot_bytes, x + (size_t)i * tb + (size_t)sl * sb, nb, &full[q]);
         }
       }
     } else if (warp == 1) {  // destinations + bulk stores
       int n = 0;
-      KMeta nxt = (int)blockIdx.x < T ? load_meta(a, idx, row_of, blockIdx.x, lane) : KMeta{0, -1};
-      for (int i = blockIdx.x; i < T; i += gridDim.x, ++n) {
+      auto tok = [&](int u) { return (int)((uint32_t)u / uns); };
+      KMeta nxt = (int)blockIdx.x < units ? load_meta(a, idx, row_of, tok(blockIdx.x), lane) : KMeta{0, -1};
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++n) {
         const int q = n % nslots;
+        const int i = tok(u), sl = u - i * ns;
         const KMeta cur = nxt;
-        if (i + (int)gridDim.x < T) nxt = load_meta(a, idx, row_of, i + gridDim.x, lane);
+        if (u + (int)gridDim.x < units) nxt = load_meta(a, idx, row_of, tok(u + gridDim.x), lane);
         int g = -1 - lane, r = -1;
         if (lane < K) {
           g = owner_tma[cur.e];
@@ -484,14 +538,15 @@ __global__ void __launch_bounds__(kTmaThreads)
         const int first_lane = __ffs(same) - 1;
         const int r_first = __shfl_sync(kFull, r, first_lane);
         const bool direct = lane < K && r >= 0 && (a.nodedup || first_lane == lane || g == s);
-        if (P > 1 && lane < K && r >= 0 && !direct && r_first >= 0)
+        if (P > 1 && sl == 0 && lane < K && r >= 0 && !direct && r_first >= 0)
           list_duplicate(a, epoch, g, i / kBlockTokens, r, r_first);
         mbar_wait_bounded(&full[q], (n / nslots) & 1, a, kSiteDispatchPipe);
         // each destination lane issues its own bulk store (per-thread bulk
-        // groups); every lane commits one group per token so the lag below
-        // counts tokens on all lanes
+        // groups); every lane commits one group per unit so the lag below
+        // counts units on all lanes
         if (direct)
-          bulk_store(a.peer[g] + act_off + (size_t)r * tb, ring + (size_t)q * slot_bytes, (uint32_t)tb);
+          bulk_store(a.peer[g] + act_off + (size_t)r * tb + (size_t)sl * sb, ring + (size_t)q * slot_bytes,
+                     unit_bytes(sl));
         bulk_commit();
         bulk_wait_read<LAG>();
         __syncwarp();
@@ -501,18 +556,18 @@ __global__ void __launch_bounds__(kTmaThreads)
       fence_proxy_async_global();
     }
     if (P > 1) {
-      // every bulk store of this CTA is complete: count its tokens into their
-      // blocks (one unit per token; tokens are strided over the grid, so the
-      // blocks complete when the last CTA gets here)
+      // every bulk store of this CTA is complete: count its units into their
+      // blocks (units are strided over the grid, so the blocks complete when
+      // the last CTA gets here)
       asm volatile("bar.sync 1, 64;" ::: "memory");  // warps 0-1 only: the others may be fanning out
       if (threadIdx.x == 0) {
         auto flush = [&](int b, uint32_t n) {
-          block_units_done(a, epoch, b, n, (uint32_t)min(kBlockTokens, T - b * kBlockTokens));
+          block_units_done(a, epoch, b, n, (uint32_t)(min(kBlockTokens, T - b * kBlockTokens) * ns));
         };
         int b_cur = -1;
         uint32_t cnt = 0;
-        for (int i = blockIdx.x; i < T; i += gridDim.x) {
-          const int b = i / kBlockTokens;
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+          const int b = (int)((uint32_t)u / uns) / kBlockTokens;
           if (b != b_cur) {
             if (cnt) flush(b_cur, cnt);
             b_cur = b;

@@ -72,6 +72,7 @@ struct fs_ctx {
   int dispatch_tma;     // 1: TMA bulk-copy dispatch engine (FUSCO_DISPATCH=tma)
   int tma_slots;        // smem ring slots per CTA of the TMA engine
   int tma_lag, tma_ctas;
+  int tma_ns, tma_sb;   // column slices per token and slice bytes (the TMA dispatch's work unit)
   size_t tma_smem;
   int pdl;              // 1: programmatic dependent launch planner -> dispatch (FUSCO_PDL=0 disables)
   int pdl_multi;        // 1: PDL for the cooperative P > 1 movers too (FUSCO_PDL_MULTI=0 disables)
@@ -102,6 +103,7 @@ struct fs_ctx {
   uint32_t* jorder_d;              // [P * nbmax]
   int push_warps;                  // warps per dispatch CTA that push before fanning out
   int claim_tokens;                // dispatch claim granularity: 1 = whole tokens, 0 = (token, slice) units
+  int fan_poll;                    // FUSCO_FAN_POLL: 1 = per-CTA cached fan-out polling
   int dbg_relaxed;                 // FUSCO_DBG_BLK=1: unordered block counts (timing experiments only)
   int disp_ctas_per_sm;            // P > 1 warp-mover grid cap (0 = occupancy)
   unsigned long long* trace_d;  // FS_NTRACE stamps when FUSCO_TRACE=1, else null
@@ -140,6 +142,7 @@ FsArgs make_args(const fs_ctx* h, int T, int idx64) {
   a.push_warps = h->push_warps;
   a.claim_tokens = h->claim_tokens;
   a.dbg_relaxed = h->dbg_relaxed;
+  a.fan_poll = h->fan_poll;
   a.blkdone = h->blkdone_d;
   a.dupcnt = h->dupcnt_d;
   a.fan_jcum = h->jcum_d;
@@ -375,7 +378,19 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
     h->tma_lag = (lag && atoi(lag) >= 4) ? 4 : 2;
     const char* ctas = getenv("FUSCO_TMA_CTAS");
     h->tma_ctas = ctas ? std::max(1, std::min(8, atoi(ctas))) : 3;
-    const int slot = tma_slot_bytes(token_bytes);
+    // column slices per token (the work unit; FUSCO_TMA_SLICES, default 1 =
+    // whole rows).  Measured: the engine is latency-bound per CTA (one unit's
+    // bulk stores in flight behind a wait_group.read lag), so smaller units
+    // cut the bytes in flight -- 2 slices made the Mixtral P=1 dispatch 40%
+    // slower -- more than they shorten the strided assignment's tail.
+    {
+      int ns = 1;
+      const char* sl = getenv("FUSCO_TMA_SLICES");
+      if (sl && atoi(sl) > 0) ns = std::min(atoi(sl), std::max(1, token_bytes / 16));
+      h->tma_sb = ((token_bytes + ns - 1) / ns + 15) & ~15;
+      h->tma_ns = (token_bytes + h->tma_sb - 1) / h->tma_sb;
+    }
+    const int slot = tma_slot_bytes(h->tma_sb);
     h->tma_slots = std::max(h->tma_lag + 2, std::min(kTmaMaxSlots, (int)((200 * 1024 / h->tma_ctas - 512) / slot)));
     h->tma_smem = 2 * kTmaMaxSlots * sizeof(uint64_t) + (size_t)h->tma_slots * slot;
     if (h->dispatch_tma) {
@@ -400,6 +415,8 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
     h->claim_tokens = cl && std::string(cl) == "token";
     const char* db = getenv("FUSCO_DBG_BLK");
     h->dbg_relaxed = db && std::string(db) == "1";
+    const char* fp = getenv("FUSCO_FAN_POLL");
+    h->fan_poll = fp && std::string(fp) == "1";
     const char* dc = getenv("FUSCO_DISP_CTAS");  // P > 1 warp mover: CTAs per SM cap
     h->disp_ctas_per_sm = dc ? std::max(1, std::min(kMaxCtasPerSm, atoi(dc))) : 0;
     const char* nd = getenv("FUSCO_NODEDUP");
@@ -627,7 +644,7 @@ int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_byte
   const bool vec16 = (h->tb % 16 == 0) && aligned(x, 16);
   if (!aligned(x, 4)) return fail(FS_EINVAL, "x must be 4-byte aligned");
   if (h->dispatch_tma && vec16) {  // unaligned x falls back to the warp mover (same grid)
-    int nslots = h->tma_slots;
+    int nslots = h->tma_slots, ns = h->tma_ns, sb = h->tma_sb;
     const void* tfn = h->tma_lag == 4 ? (const void*)dispatch_tma_kernel<4> : (const void*)dispatch_tma_kernel<2>;
     if (h->world == 1 && h->pdl) {
       // No cross-CTA or cross-rank waits at P=1: a plain launch with PDL behind
@@ -643,12 +660,12 @@ int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_byte
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       if (h->tma_lag == 4)
-        FS_CUDA(cudaLaunchKernelEx(&cfg, dispatch_tma_kernel<4>, a, (const char*)x, topk_idx, row_of, phase, nslots));
+        FS_CUDA(cudaLaunchKernelEx(&cfg, dispatch_tma_kernel<4>, a, (const char*)x, topk_idx, row_of, phase, nslots, ns, sb));
       else
-        FS_CUDA(cudaLaunchKernelEx(&cfg, dispatch_tma_kernel<2>, a, (const char*)x, topk_idx, row_of, phase, nslots));
+        FS_CUDA(cudaLaunchKernelEx(&cfg, dispatch_tma_kernel<2>, a, (const char*)x, topk_idx, row_of, phase, nslots, ns, sb));
       return FS_OK;
     }
-    void* targs[] = {&a, (void*)&x, (void*)&topk_idx, (void*)&row_of, &phase, &nslots};
+    void* targs[] = {&a, (void*)&x, (void*)&topk_idx, (void*)&row_of, &phase, &nslots, &ns, &sb};
     return launch_ex(tfn, h->move_grid, kTmaThreads, h->tma_smem, stream, targs, true, h->pdl_multi);
   }
   void* args[] = {&a, (void*)&x, (void*)&topk_idx, (void*)&row_of, &phase};

@@ -58,6 +58,7 @@ struct FsArgs {
   int push_warps;            // warps per CTA that push first (the rest fan out from the start)
   int claim_tokens;          // 1: pushers claim whole tokens (all slices), 0: (token, slice) units
   int dbg_relaxed;           // timing experiments only: block counts without release ordering
+  int fan_poll;              // 1: fan-out waits poll through a per-CTA shared-memory cache (FUSCO_FAN_POLL)
   int32_t* chunk_cnt;        // [chunks][E] scratch (per handle)
   int32_t* totals;           // [2][E] per-parity per-expert atomic totals (per handle)
   long long* stat_part;      // [2][8] per-parity atomic statistics accumulators
@@ -281,7 +282,9 @@ __device__ __forceinline__ uint32_t block_count(const FsArgs& a, uint32_t epoch,
 // every destination with its duplicate-list length.
 __device__ __forceinline__ void block_complete(const FsArgs& a, uint32_t epoch, int b) {
   const int par = (int)(epoch & 1u);
+#ifndef FUSCO_NO_BLKFENCE  // timing experiments only: drops the ordering the protocol needs
   __threadfence_system();
+#endif
   for (int g = 0; g < a.world; ++g) {
     if (g == a.rank) continue;
     const uint32_t nd = ld_relaxed_gpu_u32(a.dupcnt + ((size_t)par * a.world + g) * a.nbmax + b);

@@ -228,6 +228,25 @@ def test_engine_parity_with_oracle(engines, P, E, K, T_l, hidden, zipf):
         np.testing.assert_allclose(O.decode(res32["outs"][s], "bf16"), want, **BF16_TOL)
 
 
+@pytest.mark.parametrize("slices", [1, 3, 7])
+@pytest.mark.parametrize("P,E,K,T_l,hidden", [(1, 256, 8, 700, 7168), (4, 32, 4, 300, 1032)])
+def test_tma_dispatch_column_slices(monkeypatch, slices, P, E, K, T_l, hidden):
+    """The TMA dispatch's work unit is a (token, column slice); odd slice
+    counts leave a shorter last slice (and, at P > 1, block completion counts
+    units, not tokens) -- activations and combine stay bit-exact."""
+    monkeypatch.setenv("FUSCO_DISPATCH", "tma")
+    monkeypatch.setenv("FUSCO_TMA_SLICES", str(slices))
+    pkg, topo, pl, a, tb, payload = _cluster_case(P, E, K, T_l, hidden, "bf16", 0.9, seed=31 + slices)
+    res = _run_cluster(pkg, topo, pl, a, tb, payload, "bf16", "f64")
+    layouts, row_of = _check_layout(res, a, pl, P)
+    acts = O.dispatch(payload, layouts)
+    for g in range(P):
+        assert np.array_equal(res["acts"][g], acts[g]), f"activation/{g}"
+    for s in range(P):
+        want = O.combine(acts, row_of, a.experts, a.weights, pl.owner, res["ids"][s], "bf16")
+        assert np.array_equal(res["outs"][s], want), f"output/{s}"
+
+
 def test_engine_parity_fp32_payload(engines):
     """fp32 rows (the reference's own payload dtype) through both engines."""
     pkg, topo, pl, a, tb, payload = _cluster_case(4, 32, 4, 300, 1024, "f32", 0.7, seed=9)
