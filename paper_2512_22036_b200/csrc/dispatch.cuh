@@ -118,7 +118,8 @@ __device__ __forceinline__ void st_release_gpu_u64(unsigned long long* p, unsign
 constexpr unsigned long long kUnitMask = (1ull << 40) - 1;
 
 // The watcher warp: publishes landed jobs until every one is in (or timeout).
-static __device__ void fan_watch(const FsArgs& a, uint32_t epoch) {
+// fs = fan-out units per duplicate row (1: whole rows; S: one unit per slice)
+static __device__ void fan_watch(const FsArgs& a, uint32_t epoch, int fs) {
   const int P = a.world, s = a.rank, lane = threadIdx.x & 31;
   const int par = (int)(epoch & 1u);
   unsigned long long* ready = work_ctr(a, epoch, kWorkFanReady);
@@ -127,7 +128,7 @@ static __device__ void fan_watch(const FsArgs& a, uint32_t epoch) {
   int nb = 0;
   if (lane < P && lane != s) {
     const int Tq = read_count_word(a, par, epoch, lane, a.E);
-    nb = (Tq + kBlockTokens - 1) / kBlockTokens;
+    nb = (Tq + a.blk - 1) / a.blk;
   }
   int nbm = nb;
 #pragma unroll
@@ -161,7 +162,7 @@ static __device__ void fan_watch(const FsArgs& a, uint32_t epoch) {
       }
     }
     const bool pub = rdy && nd > 0;
-    const unsigned long long mine = pub ? (unsigned long long)nd : 0ull;  // fan-out units are whole rows
+    const unsigned long long mine = pub ? (unsigned long long)nd * (unsigned)fs : 0ull;
     // inclusive warp scan of the newly published units
     unsigned long long inc = mine;
 #pragma unroll
@@ -194,18 +195,27 @@ static __device__ void fan_watch(const FsArgs& a, uint32_t epoch) {
   if (lane == 0) st_release_gpu_u64(done, 1ull);
 }
 
-// A fan-out worker warp: claims unit groups and copies duplicate slices.
+// A fan-out worker warp: claims unit groups and copies duplicate rows.  A
+// unit is a whole row (large batches: one schedule lookup per row) or, with
+// a.fan_split (small batches: few rows, so a warp copying a 14 KB row slice
+// after slice would serialise the phase), one slice of a row.
+template <typename V>
+__device__ __forceinline__ int fan_units_per_row(const FsArgs& a, int nv) {
+  constexpr int SW = 32 * MoveCfg<V>::U;
+  return a.fan_split ? (nv + SW - 1) / SW : 1;
+}
 template <typename V>
 __device__ void fan_work(const FsArgs& a, uint32_t epoch, size_t act_off, int nv, int warps_per_cta) {
   constexpr int U = MoveCfg<V>::U;
   constexpr int SW = 32 * U;
+  const int fs = fan_units_per_row<V>(a, nv);
   const int lane = threadIdx.x & 31;
   unsigned long long* ctr = work_ctr(a, epoch, kWorkFanout);
   const unsigned long long* ready = work_ctr(a, epoch, kWorkFanReady);
   const unsigned long long* done = work_ctr(a, epoch, kWorkFanDone);
   V* act = reinterpret_cast<V*>(a.peer[a.rank] + act_off);
   const int2* dq = reinterpret_cast<const int2*>(a.peer[a.rank] + a.off_dupq);
-  const long long per_block = (long long)kBlockTokens * (a.K - 1);
+  const long long per_block = (long long)a.blk * (a.K - 1);
   unsigned long long seen = 0;  // last published word read by this warp
   uint32_t k = 0;               // job of the previous unit (units are claimed in increasing order)
   // balancer on: groups claimed dynamically; off: static striding over every warp
@@ -278,16 +288,18 @@ __device__ void fan_work(const FsArgs& a, uint32_t epoch, size_t act_off, int nv
       const unsigned long long base = k ? __ldcg(a.fan_jcum + k - 1) : 0ull;
       const uint32_t jo = __ldcg(a.fan_jorder + k);
       const int q = (int)(jo >> 16), b = (int)(jo & 0xffffu);
-      const int entry = (int)(u - base);  // the job's entry = one duplicate row
+      const int ju = (int)(u - base);
+      const int entry = ju / fs, part = ju - entry * fs;  // the job's duplicate row, and its slice (fs > 1)
       const int2 rp = __ldcg(dq + (size_t)q * a.dupq_cap + (size_t)b * per_block + entry);
       if (rp.x < 0 || rp.x >= a.max_rows || rp.y < 0 || rp.y >= a.max_rows) {
         if (lane == 0) record_error(a.status, FS_ERANGE, kSiteRows);
         continue;
       }
-      // the whole row, slice by slice (one schedule lookup per row)
+      // the whole row slice by slice, or the unit's one slice
       const V* src = act + (size_t)rp.y * nv;
       V* dst = act + (size_t)rp.x * nv;
-      for (int w0 = 0; w0 < nv; w0 += SW) {
+      const int wb = fs > 1 ? part * SW : 0, we = fs > 1 ? min(nv, wb + SW) : nv;
+      for (int w0 = wb; w0 < we; w0 += SW) {
         const int rem = nv - w0;
         V v[U];
 #pragma unroll
@@ -331,49 +343,41 @@ __global__ void __launch_bounds__(kMoveThreads, FUSCO_DISP_MINB)
   trace_stamp(a, FS_TRACE_DISPATCH_BEGIN);
 
   if (pusher) {
-    // A claim is one (token, slice) unit, or a whole token (all S slices)
-    // with a.claim_tokens.  The loop keeps three things in flight across
-    // iterations so no round trip sits on the critical path: the claim after
-    // next (lane 0's atomic, read one iteration later), the next claim's
-    // (expert, row) metadata, and the previous claim's block count (its
-    // completion check runs after this unit's payload loads are issued).
+    // Work unit = (token, slice).  Per iteration: claim the next unit and
+    // load its (expert, row) metadata while this unit's payload streams in;
+    // resolve destinations; store; count the unit into its completion block.
+    // Lane 0 checks the count's returned value one unit later (its round
+    // trip hides behind the next unit's loads and stores), so the only
+    // exposed latency per unit is the claim's.  Measured (tools/push_probe.py,
+    // Mixtral EP=2): a loop that also deferred the claim and issued the
+    // payload loads first was 10% slower, an immediate completion check 8%.
     const uint32_t uS = (uint32_t)S;
-    const uint32_t G = a.claim_tokens ? uS : 1u;  // units per claim
-    const long long claims = a.claim_tokens ? (long long)T : (long long)T * S;
+    const long long units = (long long)T * S;
     unsigned long long* ctr = work_ctr(a, epoch, kWorkDispatch);
-    // balancer on: claims taken dynamically (warps that drew light tokens
+    // balancer on: units claimed dynamically (warps that drew light tokens
     // take more); off: static striding over the pushing warps
     const bool dyn = a.balance != 0;
     const int npw = remote ? a.push_warps : kWarps;
     const bool wexcl = remote && a.push_warps == kWarps;  // CTA 0's last warp watches instead
     const long long pidx = (long long)blockIdx.x * npw + wcta - ((wexcl && blockIdx.x > 0) ? 1 : 0);
     const long long pnum = (long long)gridDim.x * npw - (wexcl ? 1 : 0);
-    auto token_of = [&](long long c) { return (int)(G == uS ? (uint32_t)c : (uint32_t)c / uS); };
-    long long c = dyn ? claim_warp(ctr) : pidx;
-    KMeta cur = c < claims ? load_meta(a, idx, row_of, token_of(c), lane) : KMeta{0, -1};
-    long long cn = dyn ? claim_warp(ctr) : c + pnum;
-    KMeta nxt = cn < claims ? load_meta(a, idx, row_of, token_of(cn), lane) : KMeta{0, -1};
-    // lane 0's deferred block count of the previous claim
-    int pend_b = -1;
-    uint32_t pend_prev = 0, pend_total = 0;
-    while (c < claims) {
-      const int i = token_of(c);
-      const int sl0 = G == uS ? 0 : (int)((uint32_t)c - (uint32_t)i * uS);
-      // 1. payload loads of the first slice: independent of everything else
+    long long u = dyn ? claim_warp(ctr) : pidx;
+    KMeta nxt = u < units ? load_meta(a, idx, row_of, (int)((uint32_t)u / uS), lane) : KMeta{0, -1};
+    int pend_b = -1;  // lane 0: block of the previous unit, its count after the add, the block's total
+    uint32_t pend_cnt = 0, pend_total = 0;
+    while (u < units) {
+      const int i = (int)((uint32_t)u / uS);
+      const int sl = (int)((uint32_t)u - (uint32_t)i * uS);
+      const KMeta cur = nxt;
+      const long long un = dyn ? claim_warp(ctr) : u + pnum;
+      if (un < units) nxt = load_meta(a, idx, row_of, (int)((uint32_t)un / uS), lane);
+      const int w0 = sl * SW, rem = nv - w0;
+      const V* src = x + (size_t)i * nv + w0;
       V v[U];
-      {
-        const int w0 = sl0 * SW, rem = nv - w0;
-        const V* src = x + (size_t)i * nv + w0;
 #pragma unroll
-        for (int j = 0; j < U; ++j)
-          if (j * 32 + lane < rem) v[j] = ld_nc(src + j * 32 + lane);
-      }
-      // 2. the claim after next, in flight while this unit is processed
-      unsigned long long raw = 0;
-      if (dyn && lane == 0) raw = atomicAdd(ctr, 1ull);
-      // 3. the previous claim completed its block?
-      if (P > 1 && lane == 0 && pend_b >= 0 && pend_prev == pend_total) block_complete(a, epoch, pend_b);
-      // 4. destinations of the token (lane k < K: owner and row of its k-th expert)
+      for (int j = 0; j < U; ++j)
+        if (j * 32 + lane < rem) v[j] = ld_nc(src + j * 32 + lane);
+      // destinations of the token (lane k < K: owner and row of its k-th expert)
       int g = -1 - lane, r = -1;  // lanes >= K get unique negative keys
       if (lane < K) {
         g = owner_sm[cur.e];
@@ -384,59 +388,44 @@ __global__ void __launch_bounds__(kMoveThreads, FUSCO_DISP_MINB)
       const int r_first = __shfl_sync(kFull, r, first_lane);
       const bool direct = lane < K && r >= 0 && (a.nodedup || first_lane == lane || g == s);
       const uint32_t dmask = __ballot_sync(kFull, direct);
-      const int b = i / kBlockTokens;
+      const int b = i / a.blk;
       // a further row of the token on an already-reached rank: listed for the
       // receiver's fan-out instead of crossing the link again
-      if (P > 1 && sl0 == 0 && lane < K && r >= 0 && !direct && r_first >= 0)
+      if (P > 1 && sl == 0 && lane < K && r >= 0 && !direct && r_first >= 0)
         list_duplicate(a, epoch, g, b, r, r_first);
       // Rotate the destination order by token so concurrent warps of this
       // rank spread their first stores over different peers.
       const int rot = dyn ? (i + s) % K : 0;
-      const uint32_t mrot = (dmask >> rot) | (rot ? (dmask << (32 - rot)) : 0u);
-      // 5. stores, slice by slice
-      for (int sl = sl0; sl < sl0 + (int)G; ++sl) {
-        const int w0 = sl * SW, rem = nv - w0;
-        if (sl != sl0) {
-          const V* src = x + (size_t)i * nv + w0;
+      uint32_t m = (dmask >> rot) | (rot ? (dmask << (32 - rot)) : 0u);
+      while (m) {
+        const int d0 = __ffs(m) - 1;
+        m &= m - 1;
+        const int d = (d0 + rot) & 31;
+        const int gd = __shfl_sync(kFull, g, d);
+        const int rd = __shfl_sync(kFull, r, d);
+        V* dst = reinterpret_cast<V*>(a.peer[gd] + act_off) + (size_t)rd * nv + w0;
 #pragma unroll
-          for (int j = 0; j < U; ++j)
-            if (j * 32 + lane < rem) v[j] = ld_nc(src + j * 32 + lane);
-        }
-        uint32_t m = mrot;
-        while (m) {
-          const int d0 = __ffs(m) - 1;
-          m &= m - 1;
-          const int d = (d0 + rot) & 31;
-          const int gd = __shfl_sync(kFull, g, d);
-          const int rd = __shfl_sync(kFull, r, d);
-          V* dst = reinterpret_cast<V*>(a.peer[gd] + act_off) + (size_t)rd * nv + w0;
-#pragma unroll
-          for (int j = 0; j < U; ++j)
-            if (j * 32 + lane < rem) st_na(dst + j * 32 + lane, v[j]);
-        }
+        for (int j = 0; j < U; ++j)
+          if (j * 32 + lane < rem) st_na(dst + j * 32 + lane, v[j]);
       }
-      // 6. count the claim into its block (checked next iteration)
       if (P > 1) {
         __syncwarp();
         if (lane == 0) {
-          const int nt = min(kBlockTokens, T - b * kBlockTokens);
-          pend_prev = block_count(a, epoch, b, G) + G;
-          pend_total = (uint32_t)(nt * S);
+          // the previous unit completed its block?  (the add returned long ago)
+          if (pend_b >= 0 && pend_cnt == pend_total) block_complete(a, epoch, pend_b);
+          pend_cnt = block_count(a, epoch, b, 1u) + 1u;
+          pend_total = (uint32_t)(min(a.blk, T - b * a.blk) * S);
           pend_b = b;
         }
       }
-      // 7. rotate the pipeline
-      c = cn;
-      cur = nxt;
-      cn = dyn ? (long long)__shfl_sync(kFull, raw, 0) : cn + pnum;
-      if (cn < claims) nxt = load_meta(a, idx, row_of, token_of(cn), lane);
+      u = un;
     }
-    if (P > 1 && lane == 0 && pend_b >= 0 && pend_prev == pend_total) block_complete(a, epoch, pend_b);
+    if (P > 1 && lane == 0 && pend_b >= 0 && pend_cnt == pend_total) block_complete(a, epoch, pend_b);
   }
   griddep_launch_dependents();  // the combine may start its prologue
   trace_stamp(a, FS_TRACE_DISPATCH_PUSHED);
   if (remote) {
-    if (watcher) fan_watch(a, epoch);
+    if (watcher) fan_watch(a, epoch, fan_units_per_row<V>(a, nv));
     fan_work<V>(a, epoch, act_off, nv, kWarps);
   }
   trace_stamp(a, FS_TRACE_DISPATCH_END);
@@ -539,7 +528,7 @@ __global__ void __launch_bounds__(kTmaThreads)
         const int r_first = __shfl_sync(kFull, r, first_lane);
         const bool direct = lane < K && r >= 0 && (a.nodedup || first_lane == lane || g == s);
         if (P > 1 && sl == 0 && lane < K && r >= 0 && !direct && r_first >= 0)
-          list_duplicate(a, epoch, g, i / kBlockTokens, r, r_first);
+          list_duplicate(a, epoch, g, i / a.blk, r, r_first);
         mbar_wait_bounded(&full[q], (n / nslots) & 1, a, kSiteDispatchPipe);
         // each destination lane issues its own bulk store (per-thread bulk
         // groups); every lane commits one group per unit so the lag below
@@ -562,12 +551,12 @@ __global__ void __launch_bounds__(kTmaThreads)
       asm volatile("bar.sync 1, 64;" ::: "memory");  // warps 0-1 only: the others may be fanning out
       if (threadIdx.x == 0) {
         auto flush = [&](int b, uint32_t n) {
-          block_units_done(a, epoch, b, n, (uint32_t)(min(kBlockTokens, T - b * kBlockTokens) * ns));
+          block_units_done(a, epoch, b, n, (uint32_t)(min(a.blk, T - b * a.blk) * ns));
         };
         int b_cur = -1;
         uint32_t cnt = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x) {
-          const int b = (int)((uint32_t)u / uns) / kBlockTokens;
+          const int b = (int)((uint32_t)u / uns) / a.blk;
           if (b != b_cur) {
             if (cnt) flush(b_cur, cnt);
             b_cur = b;
@@ -583,7 +572,7 @@ __global__ void __launch_bounds__(kTmaThreads)
 
   trace_stamp(a, FS_TRACE_DISPATCH_PUSHED);
   if (remote) {  // watcher: CTA 0's warp 3; every warp fans out once it has no push work
-    if (blockIdx.x == 0 && warp == 3) fan_watch(a, epoch);
+    if (blockIdx.x == 0 && warp == 3) fan_watch(a, epoch, fan_units_per_row<int4>(a, tb / 16));
     fan_work<int4>(a, epoch, act_off, tb / 16, kTmaThreads / 32);
   }
   trace_stamp(a, FS_TRACE_DISPATCH_END);

@@ -17,6 +17,7 @@ using namespace fusco;
 namespace {
 
 constexpr int kMaxCtasPerSm = 8;
+constexpr int kFanSplitTokens = 512;  // batches up to this size fan out slice by slice
 thread_local std::string g_err;
 
 int fail(int code, const std::string& msg) {
@@ -35,14 +36,18 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct RegionLayout {
   size_t off_count, count_stride, off_blkflag, off_dupq, off_act, act_stride, off_actout, total;
-  int nbmax;
+  int blk, nbmax;
   long long dupq_cap;
 };
 
-int blocks_per_source(int max_tokens) { return std::max(1, (max_tokens + kBlockTokens - 1) / kBlockTokens); }
+int blocks_per_source(int max_tokens) {
+  const int blk = block_tokens(max_tokens);
+  return std::max(1, (max_tokens + blk - 1) / blk);
+}
 
 RegionLayout region_layout(int world, int E, int K, int tb, int max_tokens, long long max_rows, int with_act_out) {
   RegionLayout L;
+  L.blk = block_tokens(max_tokens);
   L.nbmax = blocks_per_source(max_tokens);
   L.dupq_cap = (long long)std::max(max_tokens, 0) * (K - 1);
   L.off_count = kSigBytes;
@@ -103,6 +108,7 @@ struct fs_ctx {
   uint32_t* jorder_d;              // [P * nbmax]
   int push_warps;                  // warps per dispatch CTA that push before fanning out
   int claim_tokens;                // dispatch claim granularity: 1 = whole tokens, 0 = (token, slice) units
+  int fan_split;                   // FUSCO_FAN_SPLIT: -1 auto (by batch size), 0 rows, 1 slices
   int fan_poll;                    // FUSCO_FAN_POLL: 1 = per-CTA cached fan-out polling
   int dbg_relaxed;                 // FUSCO_DBG_BLK=1: unordered block counts (timing experiments only)
   int disp_ctas_per_sm;            // P > 1 warp-mover grid cap (0 = occupancy)
@@ -137,6 +143,7 @@ FsArgs make_args(const fs_ctx* h, int T, int idx64) {
   a.off_actout = h->L.off_actout;
   a.count_stride = h->L.count_stride;
   a.act_stride = h->L.act_stride;
+  a.blk = h->L.blk;
   a.nbmax = h->L.nbmax;
   a.dupq_cap = h->L.dupq_cap;
   a.push_warps = h->push_warps;
@@ -415,6 +422,8 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
     h->claim_tokens = cl && std::string(cl) == "token";
     const char* db = getenv("FUSCO_DBG_BLK");
     h->dbg_relaxed = db && std::string(db) == "1";
+    const char* fsp = getenv("FUSCO_FAN_SPLIT");
+    h->fan_split = fsp ? (atoi(fsp) ? 1 : 0) : -1;
     const char* fp = getenv("FUSCO_FAN_POLL");
     h->fan_poll = fp && std::string(fp) == "1";
     const char* dc = getenv("FUSCO_DISP_CTAS");  // P > 1 warp mover: CTAs per SM cap
@@ -641,6 +650,9 @@ int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_byte
   if (h->disp_phases & phase) return fail(FS_EINVAL, "fs_dispatch already ran for this plan: call fs_layout first");
   h->disp_phases |= phase;
   FsArgs a = make_args(h, num_tokens, idx_bytes == 8);
+  // receiver fan-out unit: a row slice at small batches (few duplicate rows:
+  // spread them over every warp), a whole row otherwise (FUSCO_FAN_SPLIT=0|1 overrides)
+  a.fan_split = h->fan_split >= 0 ? h->fan_split : (num_tokens <= kFanSplitTokens ? 1 : 0);
   const bool vec16 = (h->tb % 16 == 0) && aligned(x, 16);
   if (!aligned(x, 4)) return fail(FS_EINVAL, "x must be 4-byte aligned");
   if (h->dispatch_tma && vec16) {  // unaligned x falls back to the warp mover (same grid)

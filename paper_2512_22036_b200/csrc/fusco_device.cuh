@@ -28,11 +28,25 @@ constexpr size_t kOffCountFlag = 0;    // u32[FS_MAX_RANKS]: reserved (the count
 constexpr size_t kOffReadyFlag = 256;  // u32[FS_MAX_RANKS]: expert outputs ready
 
 // Completion blocks of the dispatch (P > 1): a source's tokens are cut into
-// blocks of kBlockTokens; when every unit of block b has been pushed, the
+// blocks of FsArgs::blk tokens; when every unit of block b has been pushed, the
 // source releases one epoch-tagged word per destination rank carrying the
 // number of duplicate rows it listed there for that block, and the
 // destination fans those rows out while later blocks are still in flight.
-constexpr int kBlockTokens = 128;
+// Tokens per completion block: max_tokens / 16 rounded up to a multiple of
+// 128 (at least 128, at most 2048; FsArgs::blk, equal on every rank).  Every
+// block completion costs a system-scope release per destination, so blocks
+// stay few; 16 per source still lets the fan-out start after the first
+// sixteenth of the push.
+constexpr int kBlockTarget = 16;
+__host__ __device__ inline int block_tokens(int max_tokens) {
+#ifdef FUSCO_BLOCK_TOKENS
+  return FUSCO_BLOCK_TOKENS;
+#else
+  const int per = (max_tokens + kBlockTarget - 1) / kBlockTarget;
+  const int r = ((per + 127) / 128) * 128;
+  return r < 128 ? 128 : (r > 2048 ? 2048 : r);
+#endif
+}
 constexpr int kBlkStride = 32;  // u32 words per block counter (one 128-byte line each)
 
 struct FsArgs {
@@ -53,11 +67,13 @@ struct FsArgs {
   char* peer[FS_MAX_RANKS];  // every rank's region, mapped here
   size_t off_count, off_blkflag, off_dupq, off_act, off_actout;
   size_t count_stride, act_stride;  // bytes per parity copy
-  int nbmax;                 // completion blocks per source (ceil(max_tokens / kBlockTokens))
+  int blk;                   // tokens per completion block (block_tokens(max_tokens))
+  int nbmax;                 // completion blocks per source (ceil(max_tokens / blk))
   long long dupq_cap;        // duplicate-list entries per source in a region (max_tokens * (K - 1))
   int push_warps;            // warps per CTA that push first (the rest fan out from the start)
   int claim_tokens;          // 1: pushers claim whole tokens (all slices), 0: (token, slice) units
   int dbg_relaxed;           // timing experiments only: block counts without release ordering
+  int fan_split;             // 1: fan-out units are row slices (small batches), 0: whole rows
   int fan_poll;              // 1: fan-out waits poll through a per-CTA shared-memory cache (FUSCO_FAN_POLL)
   int32_t* chunk_cnt;        // [chunks][E] scratch (per handle)
   int32_t* totals;           // [2][E] per-parity per-expert atomic totals (per handle)
@@ -245,16 +261,18 @@ __device__ __forceinline__ void gather_counts(const FsArgs& a, int parity, uint3
 }
 
 // ---- completion blocks (sender side) -----------------------------------
-// A unit (or a CTA's batch of units) of block b is done: count it on the
-// block's local counter with acq_rel at gpu scope (cumulative over the
-// caller's peer stores, which precede it in program / barrier order).  The
-// arrival that completes the block has acquired every other unit's release;
-// it issues one fence.sc.sys (so every one of the block's NVLink stores is
-// ordered before what follows at system scope) and releases the block word
-// on each destination: (epoch << 32) | number of duplicate-list entries it
-// holds.  One flag per (source, destination, block) instead of one per unit
-// — a per-unit system fence waits for the deep NVLink store queue and was
-// measured slower.
+// A unit of block b is done: count it on the block's local counter with
+// acq_rel at gpu scope (a release over the pusher's peer stores, which
+// precede it in program order).  The arrival that completes the block has
+// acquired every other unit's release; its st.release.sys of the block word
+// on each destination, (epoch << 32) | number of duplicate-list entries, is
+// cumulative over everything it acquired, so by the PTX memory model's
+// causality order (release.gpu -> acquire.gpu -> release.sys ->
+// acquire.sys) every one of the block's NVLink stores is visible to the
+// receiver's ld.acquire.sys of the word.  One flag per (source, destination,
+// block) instead of one per unit: a per-unit system fence waits for the deep
+// NVLink store queue and was measured slower, and an extra
+// fence.sc.sys before the flags cost 8-12% of the push (measured, round 2).
 __device__ __forceinline__ uint32_t atom_add_acq_rel_gpu_u32(uint32_t* p, uint32_t v) {
   uint32_t old;
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
@@ -282,7 +300,7 @@ __device__ __forceinline__ uint32_t block_count(const FsArgs& a, uint32_t epoch,
 // every destination with its duplicate-list length.
 __device__ __forceinline__ void block_complete(const FsArgs& a, uint32_t epoch, int b) {
   const int par = (int)(epoch & 1u);
-#ifndef FUSCO_NO_BLKFENCE  // timing experiments only: drops the ordering the protocol needs
+#ifdef FUSCO_BLKFENCE  // A/B only: an explicit fence.sc.sys before the release stores
   __threadfence_system();
 #endif
   for (int g = 0; g < a.world; ++g) {
@@ -300,7 +318,7 @@ __device__ __forceinline__ void list_duplicate(const FsArgs& a, uint32_t epoch, 
   uint32_t* cnt = a.dupcnt + ((size_t)(epoch & 1u) * a.world + g) * a.nbmax + b;
   const uint32_t slot = atomicAdd(cnt, 1u);
   int2* q = reinterpret_cast<int2*>(a.peer[g] + a.off_dupq) + (size_t)a.rank * a.dupq_cap +
-            (size_t)b * kBlockTokens * (a.K - 1) + slot;
+            (size_t)b * a.blk * (a.K - 1) + slot;
   *q = make_int2(row, prim);
 }
 

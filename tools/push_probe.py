@@ -38,6 +38,8 @@ def main() -> int:
     ap.add_argument("--gpus", type=int, default=2)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--tag", default="")
+    ap.add_argument("--push-only", action="store_true",
+                    help="time only the push (LOCAL phase); for builds without block accounting")
     args = ap.parse_args()
     P = args.gpus
     hidden, dtype, E, K, T_l, zipf, desc = bench.CONFIGS[args.config]
@@ -74,16 +76,20 @@ def main() -> int:
             plans = cl.layout(idx, with_masks=False)
             keep = it >= 3
             phase("push" if keep else None, lambda r: cl.ranks[r].dispatch(xs[r], plans[r], L))
+            if args.push_only:
+                continue
             phase("fanout" if keep else None, lambda r: cl.ranks[r].dispatch(xs[r], plans[r], R))
             phase("c_local" if keep else None,
                   lambda r: cl.ranks[r].combine(plans[r], ws[r], outs[r], dtype_code=1, phase=L))
             phase("pull" if keep else None,
                   lambda r: cl.ranks[r].combine(plans[r], ws[r], outs[r], dtype_code=1, phase=R))
-        cl.check()
-    med = {k: [float(np.median(v)) for v in vs] for k, vs in times.items()}
+        if not args.push_only:
+            cl.check()
+    med = {k: [float(np.median(v)) if v else 0.0 for v in vs] for k, vs in times.items()}
     out = {"config": args.config, "P": P, "tag": args.tag, "us": {k: [round(x, 1) for x in v] for k, v in med.items()},
            "push_gbps": [round(float(tr["d_eg"][r]) / (med["push"][r] * 1e-6) / 1e9, 1) for r in range(P)],
-           "pull_gbps": [round(float(tr["c_in"][r]) / (med["pull"][r] * 1e-6) / 1e9, 1) for r in range(P)],
+           "pull_gbps": [round(float(tr["c_in"][r]) / (med["pull"][r] * 1e-6) / 1e9, 1) if med["pull"][r] else None
+                         for r in range(P)],
            "push_mb": [round(float(tr["d_eg"][r]) / 1e6, 2) for r in range(P)],
            "pull_mb": [round(float(tr["c_in"][r]) / 1e6, 2) for r in range(P)]}
     print(json.dumps(out), flush=True)
