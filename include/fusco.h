@@ -207,7 +207,7 @@ int fs_trace(fs_handle_t h, uint64_t* host_out, void* stream);
 
 /* P2P/HBM copy-bandwidth probe: copies `bytes` from src to dst with the
  * same 16-byte warp copy loop the engine uses (used by bench.py to measure
- * the link/HBM peak in-run). */
+ * the link/HBM peak in-run).  src == NULL: write-only fill of dst. */
 int fs_probe_copy(int device, void* dst, const void* src, size_t bytes, int ctas, void* stream);
 
 /* All-to-all copy probe: npairs (<= 32) concurrent copies srcs[j] -> dsts[j]

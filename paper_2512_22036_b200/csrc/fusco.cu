@@ -833,7 +833,8 @@ int fs_probe_a2a(int device, void* const* dsts, const void* const* srcs, int npa
 
 int fs_probe_copy(int device, void* dst, const void* src, size_t bytes, int ctas, void* stream) {
   FS_CUDA(cudaSetDevice(device));
-  if (!dst || !src || bytes % 16 || !aligned(dst, 16) || !aligned(src, 16))
+  // src == NULL: write-only fill (the write ceiling a write-heavy mover sees)
+  if (!dst || bytes % 16 || !aligned(dst, 16) || (src && !aligned(src, 16)))
     return fail(FS_EINVAL, "fs_probe_copy: 16-byte aligned buffers and size required");
   if (ctas <= 0) return fail(FS_EINVAL, "fs_probe_copy: ctas must be > 0");
   probe_copy_kernel<<<ctas, kMoveThreads, 0, (cudaStream_t)stream>>>(

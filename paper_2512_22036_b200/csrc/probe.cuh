@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(kMoveThreads)
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       const size_t w = w0 + j * 32 + lane;
-      if (w < n16) v[j] = ld_nc(src + w);
+      if (w < n16) v[j] = src ? ld_nc(src + w) : make_int4((int)w, j, 0, 0);
     }
 #pragma unroll
     for (int j = 0; j < U; ++j) {

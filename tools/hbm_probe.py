@@ -49,6 +49,9 @@ def main():
         out[f"fs_probe_copy_{ctas}_gbs"] = best(
             lambda: _lib.check(lib.fs_probe_copy(0, c_void_p(b.data_ptr()), c_void_p(a.data_ptr()), n, ctas, st)),
             2 * n)
+    for ctas in (148 * 4, 148 * 8):
+        out[f"fs_probe_fill_{ctas}_gbs"] = best(
+            lambda: _lib.check(lib.fs_probe_copy(0, c_void_p(b.data_ptr()), c_void_p(0), n, ctas, st)), n)
     print(json.dumps({k: round(v, 1) for k, v in out.items()}))
 
 
