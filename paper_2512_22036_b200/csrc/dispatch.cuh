@@ -453,21 +453,39 @@ __host__ __device__ inline int tma_slot_bytes(int tb) { return (tb + 127) & ~127
 template <int LAG>
 __global__ void __launch_bounds__(kTmaThreads)
     dispatch_tma_kernel(FsArgs a, const char* __restrict__ x, const void* __restrict__ idx,
-                        const int32_t* __restrict__ row_of, int phase, int nslots, int ns, int sb) {
+                        const int32_t* __restrict__ row_of, int phase, int nslots, int whole, int ns, int sb) {
   TraceLast trace_last_(a, FS_TRACE_DISPATCH_LAST);
   extern __shared__ __align__(128) char tsm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
   uint64_t* empty = full + kTmaMaxSlots;
   char* ring = tsm + 2 * kTmaMaxSlots * sizeof(uint64_t);
   const int K = a.K, T = a.T, P = a.world, s = a.rank, tb = a.tb;
-  const int slot_bytes = tma_slot_bytes(sb);
+  const int slot_bytes = tma_slot_bytes(tb);  // slots hold whole rows (host: tma_smem)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // work unit = (token, column slice of sb bytes; the last one shorter):
-  // ns slices per token keep the units per CTA high enough that the tail of
-  // the strided assignment is a small fraction of the launch
-  const uint32_t uns = (uint32_t)ns;
-  const int units = T * ns;
-  auto unit_bytes = [&](int sl) { return (uint32_t)min(sb, tb - sl * sb); };
+  // Work units: tokens [0, whole) are whole rows, tokens [whole, T) are cut
+  // into ns column slices of sb bytes (the last one shorter).  Default: all
+  // whole rows (whole = T).  FUSCO_TMA_TAIL=1 sets whole = the full rounds of
+  // the strided assignment so only the last, partial round is sliced over
+  // the grid; FUSCO_TMA_SLICES=n slices every row.  Both measured no faster
+  // (DESIGN.md §10): the engine is latency-bound per CTA.
+  const int units = whole + (T - whole) * ns;
+  struct Unit {
+    int i;          // token
+    uint32_t off;   // byte offset in the row
+    uint32_t len;   // bytes
+  };
+  auto unit_of = [&](int u) -> Unit {
+    if (u < whole) return Unit{u, 0u, (uint32_t)tb};
+    const int r = u - whole;
+    const int i = whole + r / ns, sl = r - (r / ns) * ns;
+    return Unit{i, (uint32_t)(sl * sb), (uint32_t)min(sb, tb - sl * sb)};
+  };
+  // units of completion block b (P > 1 accounting)
+  auto block_units = [&](int b) -> uint32_t {
+    const int t0 = b * a.blk, t1 = min(T, t0 + a.blk);
+    const int w = max(0, min(t1, whole) - t0);
+    return (uint32_t)(w + (t1 - t0 - w) * ns);
+  };
   __shared__ int32_t owner_tma[kMaxExperts];
   // Prologue independent of the planner (launched with PDL behind it): barrier
   // init, expert table, and the first ring-full of token slices streaming in.
@@ -483,10 +501,9 @@ __global__ void __launch_bounds__(kTmaThreads)
   if ((phase & FS_PHASE_LOCAL) && threadIdx.x == 0) {
     int n = 0;
     for (int u = blockIdx.x; u < units && n < nslots; u += gridDim.x, ++n) {
-      const int i = (int)((uint32_t)u / uns), sl = u - i * ns;
-      const uint32_t nb = unit_bytes(sl);
-      mbar_arrive_expect_tx(&full[n], nb);
-      bulk_load(ring + (size_t)n * slot_bytes, x + (size_t)i * tb + (size_t)sl * sb, nb, &full[n]);
+      const Unit w = unit_of(u);
+      mbar_arrive_expect_tx(&full[n], w.len);
+      bulk_load(ring + (size_t)n * slot_bytes, x + (size_t)w.i * tb + w.off, w.len, &full[n]);
     }
   }
   griddep_wait();  // row_of / the epoch come from the planner
@@ -502,22 +519,21 @@ __global__ void __launch_bounds__(kTmaThreads)
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++n) {
           if (n < nslots) continue;
           const int q = n % nslots;
-          const int i = (int)((uint32_t)u / uns), sl = u - i * ns;
-          const uint32_t nb = unit_bytes(sl);
+          const Unit w = unit_of(u);
           mbar_wait_bounded(&empty[q], ((n / nslots) & 1) ^ 1, a, kSiteDispatchPipe);
-          mbar_arrive_expect_tx(&full[q], nb);
-          bulk_load(ring + (size_t)q * slot_bytes, x + (size_t)i * tb + (size_t)sl * sb, nb, &full[q]);
+          mbar_arrive_expect_tx(&full[q], w.len);
+          bulk_load(ring + (size_t)q * slot_bytes, x + (size_t)w.i * tb + w.off, w.len, &full[q]);
         }
       }
     } else if (warp == 1) {  // destinations + bulk stores
       int n = 0;
-      auto tok = [&](int u) { return (int)((uint32_t)u / uns); };
-      KMeta nxt = (int)blockIdx.x < units ? load_meta(a, idx, row_of, tok(blockIdx.x), lane) : KMeta{0, -1};
+      KMeta nxt = (int)blockIdx.x < units ? load_meta(a, idx, row_of, unit_of(blockIdx.x).i, lane) : KMeta{0, -1};
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++n) {
         const int q = n % nslots;
-        const int i = tok(u), sl = u - i * ns;
+        const Unit w = unit_of(u);
+        const int i = w.i;
         const KMeta cur = nxt;
-        if (u + (int)gridDim.x < units) nxt = load_meta(a, idx, row_of, tok(u + gridDim.x), lane);
+        if (u + (int)gridDim.x < units) nxt = load_meta(a, idx, row_of, unit_of(u + gridDim.x).i, lane);
         int g = -1 - lane, r = -1;
         if (lane < K) {
           g = owner_tma[cur.e];
@@ -527,15 +543,14 @@ __global__ void __launch_bounds__(kTmaThreads)
         const int first_lane = __ffs(same) - 1;
         const int r_first = __shfl_sync(kFull, r, first_lane);
         const bool direct = lane < K && r >= 0 && (a.nodedup || first_lane == lane || g == s);
-        if (P > 1 && sl == 0 && lane < K && r >= 0 && !direct && r_first >= 0)
+        if (P > 1 && w.off == 0 && lane < K && r >= 0 && !direct && r_first >= 0)
           list_duplicate(a, epoch, g, i / a.blk, r, r_first);
         mbar_wait_bounded(&full[q], (n / nslots) & 1, a, kSiteDispatchPipe);
         // each destination lane issues its own bulk store (per-thread bulk
         // groups); every lane commits one group per unit so the lag below
         // counts units on all lanes
         if (direct)
-          bulk_store(a.peer[g] + act_off + (size_t)r * tb + (size_t)sl * sb, ring + (size_t)q * slot_bytes,
-                     unit_bytes(sl));
+          bulk_store(a.peer[g] + act_off + (size_t)r * tb + w.off, ring + (size_t)q * slot_bytes, w.len);
         bulk_commit();
         bulk_wait_read<LAG>();
         __syncwarp();
@@ -551,12 +566,12 @@ __global__ void __launch_bounds__(kTmaThreads)
       asm volatile("bar.sync 1, 64;" ::: "memory");  // warps 0-1 only: the others may be fanning out
       if (threadIdx.x == 0) {
         auto flush = [&](int b, uint32_t n) {
-          block_units_done(a, epoch, b, n, (uint32_t)(min(a.blk, T - b * a.blk) * ns));
+          block_units_done(a, epoch, b, n, block_units(b));
         };
         int b_cur = -1;
         uint32_t cnt = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x) {
-          const int b = (int)((uint32_t)u / uns) / a.blk;
+          const int b = unit_of(u).i / a.blk;
           if (b != b_cur) {
             if (cnt) flush(b_cur, cnt);
             b_cur = b;

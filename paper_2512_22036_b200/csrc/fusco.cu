@@ -77,7 +77,9 @@ struct fs_ctx {
   int dispatch_tma;     // 1: TMA bulk-copy dispatch engine (FUSCO_DISPATCH=tma)
   int tma_slots;        // smem ring slots per CTA of the TMA engine
   int tma_lag, tma_ctas;
-  int tma_ns, tma_sb;   // column slices per token and slice bytes (the TMA dispatch's work unit)
+  int tma_sb;           // slot payload bytes (a whole row)
+  int tma_slices;       // FUSCO_TMA_SLICES: > 0 cuts every row into this many slices (A/B)
+  int tma_tail;         // 1: slice the last partial round's rows (FUSCO_TMA_TAIL=1)
   size_t tma_smem;
   int pdl;              // 1: programmatic dependent launch planner -> dispatch (FUSCO_PDL=0 disables)
   int pdl_multi;        // 1: PDL for the cooperative P > 1 movers too (FUSCO_PDL_MULTI=0 disables)
@@ -385,17 +387,19 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
     h->tma_lag = (lag && atoi(lag) >= 4) ? 4 : 2;
     const char* ctas = getenv("FUSCO_TMA_CTAS");
     h->tma_ctas = ctas ? std::max(1, std::min(8, atoi(ctas))) : 3;
-    // column slices per token (the work unit; FUSCO_TMA_SLICES, default 1 =
-    // whole rows).  Measured: the engine is latency-bound per CTA (one unit's
-    // bulk stores in flight behind a wait_group.read lag), so smaller units
-    // cut the bytes in flight -- 2 slices made the Mixtral P=1 dispatch 40%
-    // slower -- more than they shorten the strided assignment's tail.
+    // Work unit: whole rows (default).  Measured alternatives (A/B knobs):
+    // FUSCO_TMA_TAIL=1 cuts only the last partial round of the strided
+    // assignment into column slices (neutral: DeepSeek-V3 96.8 vs 97.2 us,
+    // Mixtral 41.2 vs 40.2 -- the strided tail is not what bounds the
+    // launch); FUSCO_TMA_SLICES=n cuts every row into n slices (slower: the
+    // engine is latency-bound per CTA, 2 slices made the Mixtral P=1
+    // dispatch 40% slower).
     {
-      int ns = 1;
       const char* sl = getenv("FUSCO_TMA_SLICES");
-      if (sl && atoi(sl) > 0) ns = std::min(atoi(sl), std::max(1, token_bytes / 16));
-      h->tma_sb = ((token_bytes + ns - 1) / ns + 15) & ~15;
-      h->tma_ns = (token_bytes + h->tma_sb - 1) / h->tma_sb;
+      h->tma_slices = (sl && atoi(sl) > 0) ? std::min(atoi(sl), std::max(1, token_bytes / 16)) : 0;
+      const char* tl = getenv("FUSCO_TMA_TAIL");
+      h->tma_tail = tl && std::string(tl) == "1";
+      h->tma_sb = token_bytes;  // slots hold whole rows
     }
     const int slot = tma_slot_bytes(h->tma_sb);
     h->tma_slots = std::max(h->tma_lag + 2, std::min(kTmaMaxSlots, (int)((200 * 1024 / h->tma_ctas - 512) / slot)));
@@ -656,7 +660,24 @@ int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_byte
   const bool vec16 = (h->tb % 16 == 0) && aligned(x, 16);
   if (!aligned(x, 4)) return fail(FS_EINVAL, "x must be 4-byte aligned");
   if (h->dispatch_tma && vec16) {  // unaligned x falls back to the warp mover (same grid)
-    int nslots = h->tma_slots, ns = h->tma_ns, sb = h->tma_sb;
+    int nslots = h->tma_slots, whole = num_tokens, ns = 1, sb = h->tb;
+    {
+      // rows of the full rounds stay whole; the last round's rows are sliced
+      // so they spread over the grid (>= 2 KiB per slice)
+      const int grid = h->move_grid;
+      const int max_ns = std::max(1, h->tb / 2048);
+      if (h->tma_slices > 0) {
+        whole = 0;
+        ns = h->tma_slices;
+      } else if (h->tma_tail && num_tokens > 0) {
+        whole = (num_tokens / grid) * grid;
+        const int tail = num_tokens - whole;
+        if (tail > 0) ns = std::min(max_ns, (grid + tail - 1) / tail);
+      }
+      sb = ((h->tb + ns - 1) / ns + 15) & ~15;
+      ns = (h->tb + sb - 1) / sb;
+      if (ns == 1) whole = num_tokens;
+    }
     const void* tfn = h->tma_lag == 4 ? (const void*)dispatch_tma_kernel<4> : (const void*)dispatch_tma_kernel<2>;
     if (h->world == 1 && h->pdl) {
       // No cross-CTA or cross-rank waits at P=1: a plain launch with PDL behind
@@ -672,12 +693,12 @@ int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_byte
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       if (h->tma_lag == 4)
-        FS_CUDA(cudaLaunchKernelEx(&cfg, dispatch_tma_kernel<4>, a, (const char*)x, topk_idx, row_of, phase, nslots, ns, sb));
+        FS_CUDA(cudaLaunchKernelEx(&cfg, dispatch_tma_kernel<4>, a, (const char*)x, topk_idx, row_of, phase, nslots, whole, ns, sb));
       else
-        FS_CUDA(cudaLaunchKernelEx(&cfg, dispatch_tma_kernel<2>, a, (const char*)x, topk_idx, row_of, phase, nslots, ns, sb));
+        FS_CUDA(cudaLaunchKernelEx(&cfg, dispatch_tma_kernel<2>, a, (const char*)x, topk_idx, row_of, phase, nslots, whole, ns, sb));
       return FS_OK;
     }
-    void* targs[] = {&a, (void*)&x, (void*)&topk_idx, (void*)&row_of, &phase, &nslots, &ns, &sb};
+    void* targs[] = {&a, (void*)&x, (void*)&topk_idx, (void*)&row_of, &phase, &nslots, &whole, &ns, &sb};
     return launch_ex(tfn, h->move_grid, kTmaThreads, h->tma_smem, stream, targs, true, h->pdl_multi);
   }
   void* args[] = {&a, (void*)&x, (void*)&topk_idx, (void*)&row_of, &phase};

@@ -228,14 +228,20 @@ def test_engine_parity_with_oracle(engines, P, E, K, T_l, hidden, zipf):
         np.testing.assert_allclose(O.decode(res32["outs"][s], "bf16"), want, **BF16_TOL)
 
 
-@pytest.mark.parametrize("slices", [1, 3, 7])
-@pytest.mark.parametrize("P,E,K,T_l,hidden", [(1, 256, 8, 700, 7168), (4, 32, 4, 300, 1032)])
+@pytest.mark.parametrize("slices", [0, 1, 3, 7])
+@pytest.mark.parametrize("P,E,K,T_l,hidden", [(1, 256, 8, 700, 7168), (1, 8, 2, 1500, 4096),
+                                             (4, 32, 4, 300, 1032)])
 def test_tma_dispatch_column_slices(monkeypatch, slices, P, E, K, T_l, hidden):
-    """The TMA dispatch's work unit is a (token, column slice); odd slice
-    counts leave a shorter last slice (and, at P > 1, block completion counts
-    units, not tokens) -- activations and combine stay bit-exact."""
+    """The TMA dispatch's work unit is a whole row or a (token, column slice):
+    slices=0 slices only the last partial round of the grid (FUSCO_TMA_TAIL=1),
+    n > 0 slices every row (odd n leaves a shorter last slice).  At P > 1
+    block completion counts units, not tokens.  Activations and the combine
+    stay bit-exact."""
     monkeypatch.setenv("FUSCO_DISPATCH", "tma")
-    monkeypatch.setenv("FUSCO_TMA_SLICES", str(slices))
+    if slices:
+        monkeypatch.setenv("FUSCO_TMA_SLICES", str(slices))
+    else:
+        monkeypatch.setenv("FUSCO_TMA_TAIL", "1")
     pkg, topo, pl, a, tb, payload = _cluster_case(P, E, K, T_l, hidden, "bf16", 0.9, seed=31 + slices)
     res = _run_cluster(pkg, topo, pl, a, tb, payload, "bf16", "f64")
     layouts, row_of = _check_layout(res, a, pl, P)
