@@ -84,6 +84,7 @@ extern "C" {
 #define FS_TRACE_LAYOUT_PUBLISH 3
 #define FS_TRACE_LAYOUT_WAIT 4
 #define FS_TRACE_LAYOUT_END 5
+#define FS_TRACE_DISPATCH_SIGNAL 7 /* sender: the last completion block released (any CTA) */
 #define FS_TRACE_DISPATCH_BEGIN 8
 #define FS_TRACE_DISPATCH_PUSHED 9
 #define FS_TRACE_DISPATCH_ARRIVED 10
@@ -209,6 +210,14 @@ int fs_trace(fs_handle_t h, uint64_t* host_out, void* stream);
  * same 16-byte warp copy loop the engine uses (used by bench.py to measure
  * the link/HBM peak in-run).  src == NULL: write-only fill of dst. */
 int fs_probe_copy(int device, void* dst, const void* src, size_t bytes, int ctas, void* stream);
+
+/* Row-scatter probe, the dispatch's HBM write pattern without its metadata:
+ * warp w reads row src[r] (r = w, w + warps, ...; nrows_src rows) and writes
+ * it to the `fanout` rows perm[r * fanout + j] of dst (device int32 array),
+ * row_bytes each (multiple of 16).  src == NULL: write-only.  Used by
+ * tools/hbm_probe.py to measure the ceiling of the P=1 dispatch's pattern. */
+int fs_probe_scatter(int device, void* dst, const void* src, const int32_t* perm, int nrows_src, int fanout,
+                     int row_bytes, int ctas, void* stream);
 
 /* All-to-all copy probe: npairs (<= 32) concurrent copies srcs[j] -> dsts[j]
  * of `bytes` each (host arrays of device pointers, local or peer-mapped).

@@ -66,6 +66,7 @@ SIGNATURES = {
     "fs_trace": (c_int, [c_void_p, c_void_p, c_void_p]),
     "fs_probe_a2a": (c_int, [c_int, c_void_p, c_void_p, c_int, c_size_t, c_int, c_int, c_void_p]),
     "fs_probe_copy": (c_int, [c_int, c_void_p, c_void_p, c_size_t, c_int, c_void_p]),
+    "fs_probe_scatter": (c_int, [c_int, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p]),
 }
 
 _lib = None

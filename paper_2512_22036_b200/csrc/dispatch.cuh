@@ -337,30 +337,180 @@ __global__ void __launch_bounds__(kMoveThreads, FUSCO_DISP_MINB)
   __shared__ int32_t owner_sm[kMaxExperts];
   if (phase & FS_PHASE_REMOTE) fan_poll_init();
   if (phase & FS_PHASE_LOCAL) load_owner_table(a, owner_sm);  // static table: before the PDL wait
+  const uint32_t uS = (uint32_t)S;
+  const long long units = (long long)T * S;
+  // pushing warps and this warp's static index among them
+  const int npw = remote ? a.push_warps : kWarps;
+  const bool wexcl = remote && a.push_warps == kWarps;  // CTA 0's last warp watches instead
+  const long long pidx = (long long)blockIdx.x * npw + wcta - ((wexcl && blockIdx.x > 0) ? 1 : 0);
+  const long long pnum = (long long)gridDim.x * npw - (wexcl ? 1 : 0);
+  // Small batches (every pushing warp has at most one unit, e.g. decode):
+  // static assignment, no claim atomic, and the unit's payload rows and
+  // expert ids -- inputs, not planner outputs -- are loaded before the PDL
+  // wait, so they stream in while the planner finishes.  Only row_of waits.
+  const bool small = pusher && units <= pnum;
+  V v[U];
+  KMeta cur{0, -1};
+  if (small && pidx < units) {
+    const int i = (int)((uint32_t)pidx / uS), sl = (int)((uint32_t)pidx - (uint32_t)i * uS);
+    const int w0 = sl * SW, rem = nv - w0;
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (j * 32 + lane < rem) v[j] = ld_nc(x + (size_t)i * nv + w0 + j * 32 + lane);
+    if (lane < K) {
+      const long long e = load_idx(idx, (size_t)i * K + lane, a.idx64);
+      cur.e = (e < 0 || e >= a.E) ? 0 : (int)e;
+    }
+  }
   griddep_wait();  // row_of / the epoch come from the planner
   const uint32_t epoch = load_epoch(a);
   const size_t act_off = a.off_act;
   trace_stamp(a, FS_TRACE_DISPATCH_BEGIN);
 
-  if (pusher) {
-    // Work unit = (token, slice).  Per iteration: claim the next unit and
-    // load its (expert, row) metadata while this unit's payload streams in;
-    // resolve destinations; store; count the unit into its completion block.
-    // Lane 0 checks the count's returned value one unit later (its round
-    // trip hides behind the next unit's loads and stores), so the only
-    // exposed latency per unit is the claim's.  Measured (tools/push_probe.py,
-    // Mixtral EP=2): a loop that also deferred the claim and issued the
-    // payload loads first was 10% slower, an immediate completion check 8%.
-    const uint32_t uS = (uint32_t)S;
-    const long long units = (long long)T * S;
+  // One unit (token i, slice sl) whose payload is in v and whose k-th expert
+  // (and destination row) lane k holds in m: resolve destinations, list
+  // duplicates, store.  Returns the unit's completion block.
+  auto push_unit = [&](int i, int sl, const KMeta& m) -> int {
+    const int w0 = sl * SW, rem = nv - w0;
+    // destinations of the token (lane k < K: owner and row of its k-th expert)
+    int g = -1 - lane, r = -1;  // lanes >= K get unique negative keys
+    if (lane < K) {
+      g = owner_sm[m.e];
+      r = (m.r < 0 || m.r >= a.max_rows) ? -1 : m.r;
+    }
+    const uint32_t same = __match_any_sync(kFull, g);
+    const int first_lane = __ffs(same) - 1;
+    const int r_first = __shfl_sync(kFull, r, first_lane);
+    const bool direct = lane < K && r >= 0 && (a.nodedup || first_lane == lane || g == s);
+    const uint32_t dmask = __ballot_sync(kFull, direct);
+    const int b = i / a.blk;
+    // a further row of the token on an already-reached rank: listed for the
+    // receiver's fan-out instead of crossing the link again
+    if (P > 1 && sl == 0 && lane < K && r >= 0 && !direct && r_first >= 0)
+      list_duplicate(a, epoch, g, b, r, r_first);
+    // Rotate the destination order by token so concurrent warps of this
+    // rank spread their first stores over different peers.
+    const int rot = a.balance ? (i + s) % K : 0;
+    uint32_t mm = (dmask >> rot) | (rot ? (dmask << (32 - rot)) : 0u);
+    while (mm) {
+      const int d0 = __ffs(mm) - 1;
+      mm &= mm - 1;
+      const int d = (d0 + rot) & 31;
+      const int gd = __shfl_sync(kFull, g, d);
+      const int rd = __shfl_sync(kFull, r, d);
+      V* dst = reinterpret_cast<V*>(a.peer[gd] + act_off) + (size_t)rd * nv + w0;
+#pragma unroll
+      for (int j = 0; j < U; ++j)
+        if (j * 32 + lane < rem) st_na(dst + j * 32 + lane, v[j]);
+    }
+    return b;
+  };
+
+  // pushing warps of this CTA (CTA 0's last warp watches at P > 1) and the
+  // CTA's first static unit
+  const int rcta = (wexcl && blockIdx.x == 0) ? kWarps - 1 : npw;
+  const long long cta_first = pidx - wcta;
+  // Completion accounting per CTA round (a.push_rounds, FUSCO_PUSH_ROUNDS=1):
+  // the CTA's pushing warps each push one unit of a run of rcta consecutive
+  // units, meet at a named barrier, and thread 0 counts the run into its (at
+  // most two) blocks with one acq_rel atomic each -- the release that orders
+  // the round's peer stores before the count (cumulative over the barrier).
+  // Measured against the default per-unit count (the per-warp loop below):
+  // 1-2 % slower at large batches (the barrier waits for the round's slowest
+  // warp), equal at decode -- the per-unit release is not what bounds the push.
+  // Thread 0 checks a round's counts one round later (pending arrays).
+  int pb[2] = {-1, -1};
+  uint32_t pc[2] = {0, 0}, pt[2] = {0, 0};
+  auto count_run = [&](long long base, int n) {  // thread 0: count units [base, base + n)
+    if (n <= 0) return;
+    for (int q = 0; q < 2; ++q)
+      if (pb[q] >= 0 && pc[q] == pt[q]) block_complete(a, epoch, pb[q]);
+    pb[0] = pb[1] = -1;
+    long long u0 = base;
+    const long long u1 = base + n;
+    for (int q = 0; q < 2 && u0 < u1; ++q) {
+      const int b = (int)((uint32_t)u0 / uS) / a.blk;
+      const long long bend = (long long)(b + 1) * a.blk * S;
+      const uint32_t c = (uint32_t)((u1 < bend ? u1 : bend) - u0);
+      pc[q] = block_count(a, epoch, b, c) + c;
+      pt[q] = (uint32_t)(min(a.blk, T - b * a.blk) * S);
+      pb[q] = b;
+      u0 += c;
+    }
+  };
+  auto finish_runs = [&]() {
+    for (int q = 0; q < 2; ++q)
+      if (pb[q] >= 0 && pc[q] == pt[q]) block_complete(a, epoch, pb[q]);
+  };
+  auto pusher_bar = [&]() { asm volatile("bar.sync 2, %0;" ::"r"(rcta * 32) : "memory"); };
+
+  if (small) {
+    // one round: this CTA's units [cta_first, cta_first + rcta)
+    if (pidx < units) {
+      const int i = (int)((uint32_t)pidx / uS), sl = (int)((uint32_t)pidx - (uint32_t)i * uS);
+      if (lane < K) cur.r = row_of[(size_t)i * K + lane];
+      const int b = push_unit(i, sl, cur);
+      if (P > 1 && !a.push_rounds) {
+        __syncwarp();
+        if (lane == 0) block_units_done(a, epoch, b, 1u, (uint32_t)(min(a.blk, T - b * a.blk) * S));
+      }
+    }
+    if (P > 1 && a.push_rounds) {
+      pusher_bar();
+      if (threadIdx.x == 0) {
+        count_run(cta_first, (int)min((long long)rcta, units - cta_first));
+        finish_runs();
+      }
+    }
+  } else if (pusher && a.push_rounds) {
+    __shared__ long long rbase[3];  // round bases, claimed two rounds ahead (triple buffer)
+    unsigned long long* ctr = work_ctr(a, epoch, kWorkDispatch);
+    const bool dyn = a.balance != 0;
+    auto round_base = [&](long long r) -> long long {  // static striding: the CTA's r-th run
+      return cta_first + r * pnum;
+    };
+    if (threadIdx.x == 0 && dyn) {
+      rbase[0] = (long long)atomicAdd(ctr, (unsigned long long)rcta);
+      rbase[1] = (long long)atomicAdd(ctr, (unsigned long long)rcta);
+    }
+    pusher_bar();
+    long long base = dyn ? rbase[0] : round_base(0);
+    long long nbase = dyn ? rbase[1] : round_base(1);
+    KMeta nxt = base + wcta < units ? load_meta(a, idx, row_of, (int)((uint32_t)(base + wcta) / uS), lane)
+                                    : KMeta{0, -1};
+    for (long long r = 0; base < units; ++r) {
+      unsigned long long claim = 0;
+      if (threadIdx.x == 0 && dyn) claim = atomicAdd(ctr, (unsigned long long)rcta);  // round r + 2
+      const long long u = base + wcta;
+      cur = nxt;
+      if (nbase + wcta < units) nxt = load_meta(a, idx, row_of, (int)((uint32_t)(nbase + wcta) / uS), lane);
+      if (u < units) {
+        const int i = (int)((uint32_t)u / uS), sl = (int)((uint32_t)u - (uint32_t)i * uS);
+        const int w0 = sl * SW, rem = nv - w0;
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (j * 32 + lane < rem) v[j] = ld_nc(x + (size_t)i * nv + w0 + j * 32 + lane);
+        push_unit(i, sl, cur);
+      }
+      if (threadIdx.x == 0 && dyn) rbase[(r + 2) % 3] = (long long)claim;
+      pusher_bar();  // the round's stores are issued; rbase[(r + 2) % 3] is visible
+      if (P > 1 && threadIdx.x == 0) count_run(base, (int)min((long long)rcta, units - base));
+      base = nbase;
+      nbase = dyn ? rbase[(r + 2) % 3] : round_base(r + 2);
+    }
+    if (P > 1 && threadIdx.x == 0) finish_runs();
+  } else if (pusher) {
+    // Per-warp loop (default).  Work unit = (token, slice).  Per
+    // iteration: claim the next unit and load its (expert, row) metadata
+    // while this unit's payload streams in; resolve destinations; store;
+    // count the unit into its completion block.  Lane 0 checks the count's
+    // returned value one unit later.  Measured (tools/push_probe.py, Mixtral
+    // EP=2): a loop that also deferred the claim and issued the payload loads
+    // first was 10% slower, an immediate completion check 8%.
     unsigned long long* ctr = work_ctr(a, epoch, kWorkDispatch);
     // balancer on: units claimed dynamically (warps that drew light tokens
     // take more); off: static striding over the pushing warps
     const bool dyn = a.balance != 0;
-    const int npw = remote ? a.push_warps : kWarps;
-    const bool wexcl = remote && a.push_warps == kWarps;  // CTA 0's last warp watches instead
-    const long long pidx = (long long)blockIdx.x * npw + wcta - ((wexcl && blockIdx.x > 0) ? 1 : 0);
-    const long long pnum = (long long)gridDim.x * npw - (wexcl ? 1 : 0);
     long long u = dyn ? claim_warp(ctr) : pidx;
     KMeta nxt = u < units ? load_meta(a, idx, row_of, (int)((uint32_t)u / uS), lane) : KMeta{0, -1};
     int pend_b = -1;  // lane 0: block of the previous unit, its count after the add, the block's total
@@ -368,46 +518,14 @@ __global__ void __launch_bounds__(kMoveThreads, FUSCO_DISP_MINB)
     while (u < units) {
       const int i = (int)((uint32_t)u / uS);
       const int sl = (int)((uint32_t)u - (uint32_t)i * uS);
-      const KMeta cur = nxt;
+      cur = nxt;
       const long long un = dyn ? claim_warp(ctr) : u + pnum;
       if (un < units) nxt = load_meta(a, idx, row_of, (int)((uint32_t)un / uS), lane);
       const int w0 = sl * SW, rem = nv - w0;
-      const V* src = x + (size_t)i * nv + w0;
-      V v[U];
 #pragma unroll
       for (int j = 0; j < U; ++j)
-        if (j * 32 + lane < rem) v[j] = ld_nc(src + j * 32 + lane);
-      // destinations of the token (lane k < K: owner and row of its k-th expert)
-      int g = -1 - lane, r = -1;  // lanes >= K get unique negative keys
-      if (lane < K) {
-        g = owner_sm[cur.e];
-        r = (cur.r < 0 || cur.r >= a.max_rows) ? -1 : cur.r;
-      }
-      const uint32_t same = __match_any_sync(kFull, g);
-      const int first_lane = __ffs(same) - 1;
-      const int r_first = __shfl_sync(kFull, r, first_lane);
-      const bool direct = lane < K && r >= 0 && (a.nodedup || first_lane == lane || g == s);
-      const uint32_t dmask = __ballot_sync(kFull, direct);
-      const int b = i / a.blk;
-      // a further row of the token on an already-reached rank: listed for the
-      // receiver's fan-out instead of crossing the link again
-      if (P > 1 && sl == 0 && lane < K && r >= 0 && !direct && r_first >= 0)
-        list_duplicate(a, epoch, g, b, r, r_first);
-      // Rotate the destination order by token so concurrent warps of this
-      // rank spread their first stores over different peers.
-      const int rot = dyn ? (i + s) % K : 0;
-      uint32_t m = (dmask >> rot) | (rot ? (dmask << (32 - rot)) : 0u);
-      while (m) {
-        const int d0 = __ffs(m) - 1;
-        m &= m - 1;
-        const int d = (d0 + rot) & 31;
-        const int gd = __shfl_sync(kFull, g, d);
-        const int rd = __shfl_sync(kFull, r, d);
-        V* dst = reinterpret_cast<V*>(a.peer[gd] + act_off) + (size_t)rd * nv + w0;
-#pragma unroll
-        for (int j = 0; j < U; ++j)
-          if (j * 32 + lane < rem) st_na(dst + j * 32 + lane, v[j]);
-      }
+        if (j * 32 + lane < rem) v[j] = ld_nc(x + (size_t)i * nv + w0 + j * 32 + lane);
+      const int b = push_unit(i, sl, cur);
       if (P > 1) {
         __syncwarp();
         if (lane == 0) {

@@ -110,6 +110,7 @@ struct fs_ctx {
   uint32_t* jorder_d;              // [P * nbmax]
   int push_warps;                  // warps per dispatch CTA that push before fanning out
   int claim_tokens;                // dispatch claim granularity: 1 = whole tokens, 0 = (token, slice) units
+  int push_rounds;                 // FUSCO_PUSH_ROUNDS=1: per-CTA-round completion counts (A/B; default per unit)
   int fan_split;                   // FUSCO_FAN_SPLIT: -1 auto (by batch size), 0 rows, 1 slices
   int fan_poll;                    // FUSCO_FAN_POLL: 1 = per-CTA cached fan-out polling
   int dbg_relaxed;                 // FUSCO_DBG_BLK=1: unordered block counts (timing experiments only)
@@ -152,6 +153,7 @@ FsArgs make_args(const fs_ctx* h, int T, int idx64) {
   a.claim_tokens = h->claim_tokens;
   a.dbg_relaxed = h->dbg_relaxed;
   a.fan_poll = h->fan_poll;
+  a.push_rounds = h->push_rounds;
   a.blkdone = h->blkdone_d;
   a.dupcnt = h->dupcnt_d;
   a.fan_jcum = h->jcum_d;
@@ -426,6 +428,8 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
     h->claim_tokens = cl && std::string(cl) == "token";
     const char* db = getenv("FUSCO_DBG_BLK");
     h->dbg_relaxed = db && std::string(db) == "1";
+    const char* pr = getenv("FUSCO_PUSH_ROUNDS");
+    h->push_rounds = pr && std::string(pr) == "1";
     const char* fsp = getenv("FUSCO_FAN_SPLIT");
     h->fan_split = fsp ? (atoi(fsp) ? 1 : 0) : -1;
     const char* fp = getenv("FUSCO_FAN_POLL");
@@ -860,6 +864,18 @@ int fs_probe_copy(int device, void* dst, const void* src, size_t bytes, int ctas
   if (ctas <= 0) return fail(FS_EINVAL, "fs_probe_copy: ctas must be > 0");
   probe_copy_kernel<<<ctas, kMoveThreads, 0, (cudaStream_t)stream>>>(
       reinterpret_cast<int4*>(dst), reinterpret_cast<const int4*>(src), bytes / 16);
+  FS_CUDA(cudaGetLastError());
+  return FS_OK;
+}
+
+int fs_probe_scatter(int device, void* dst, const void* src, const int32_t* perm, int nrows_src, int fanout,
+                     int row_bytes, int ctas, void* stream) {
+  FS_CUDA(cudaSetDevice(device));
+  if (!dst || !perm || row_bytes <= 0 || row_bytes % 16 || !aligned(dst, 16) || (src && !aligned(src, 16)) ||
+      nrows_src < 0 || fanout <= 0 || ctas <= 0)
+    return fail(FS_EINVAL, "fs_probe_scatter: bad arguments");
+  probe_scatter_kernel<<<ctas, kMoveThreads, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<int4*>(dst), reinterpret_cast<const int4*>(src), perm, nrows_src, fanout, row_bytes / 16);
   FS_CUDA(cudaGetLastError());
   return FS_OK;
 }

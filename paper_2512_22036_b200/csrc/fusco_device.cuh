@@ -73,6 +73,7 @@ struct FsArgs {
   int push_warps;            // warps per CTA that push first (the rest fan out from the start)
   int claim_tokens;          // 1: pushers claim whole tokens (all slices), 0: (token, slice) units
   int dbg_relaxed;           // timing experiments only: block counts without release ordering
+  int push_rounds;           // 1: completion counted per CTA round (FUSCO_PUSH_ROUNDS=1), 0: per unit (default)
   int fan_split;             // 1: fan-out units are row slices (small batches), 0: whole rows
   int fan_poll;              // 1: fan-out waits poll through a per-CTA shared-memory cache (FUSCO_FAN_POLL)
   int32_t* chunk_cnt;        // [chunks][E] scratch (per handle)
@@ -308,6 +309,7 @@ __device__ __forceinline__ void block_complete(const FsArgs& a, uint32_t epoch, 
     const uint32_t nd = ld_relaxed_gpu_u32(a.dupcnt + ((size_t)par * a.world + g) * a.nbmax + b);
     st_release_sys_u64(blkflag_ptr(a, g, a.rank, b), ((unsigned long long)epoch << 32) | nd);
   }
+  if (a.trace != nullptr && b == (a.T - 1) / a.blk) a.trace[FS_TRACE_DISPATCH_SIGNAL] = globaltimer();
 }
 __device__ __forceinline__ void block_units_done(const FsArgs& a, uint32_t epoch, int b, uint32_t n,
                                                  uint32_t total) {

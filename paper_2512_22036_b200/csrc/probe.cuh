@@ -31,6 +31,35 @@ __global__ void __launch_bounds__(kMoveThreads)
   }
 }
 
+// Row-scatter probe: the P=1 dispatch's pattern (read a row once, write it to
+// `fanout` scattered rows) with the engine's 16-byte warp moves, no metadata.
+__global__ void __launch_bounds__(kMoveThreads)
+    probe_scatter_kernel(int4* __restrict__ dst, const int4* __restrict__ src, const int32_t* __restrict__ perm,
+                         int nrows, int fanout, int nv) {
+  constexpr int U = 8;
+  const int lane = threadIdx.x & 31;
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+  for (long long r = gw; r < nrows; r += nw) {
+    for (int w0 = 0; w0 < nv; w0 += 32 * U) {
+      int4 v[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int w = w0 + j * 32 + lane;
+        if (w < nv) v[j] = src ? ld_nc(src + r * nv + w) : make_int4(w, j, 0, 0);
+      }
+      for (int f = 0; f < fanout; ++f) {
+        int4* d = dst + (size_t)perm[r * fanout + f] * nv;
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const int w = w0 + j * 32 + lane;
+          if (w < nv) st_na(d + w, v[j]);
+        }
+      }
+    }
+  }
+}
+
 // ===========================================================================
 // All-to-all copy probe: pairs j = 0..n-1 copy src[j] -> dst[j] concurrently
 // (chunks interleaved over CTAs so every pair progresses at once).  With

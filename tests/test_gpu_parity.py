@@ -253,6 +253,23 @@ def test_tma_dispatch_column_slices(monkeypatch, slices, P, E, K, T_l, hidden):
         assert np.array_equal(res["outs"][s], want), f"output/{s}"
 
 
+@pytest.mark.parametrize("P,E,K,T_l,hidden", [(4, 8, 2, 1024, 4096), (8, 256, 8, 128, 7168), (2, 16, 4, 333, 1024)])
+def test_push_rounds_parity(monkeypatch, P, E, K, T_l, hidden):
+    """Per-CTA-round completion counting (FUSCO_PUSH_ROUNDS=1, the A/B variant
+    of the per-unit count): same layout, activations and combine, bit-exact."""
+    monkeypatch.setenv("FUSCO_DISPATCH", "warp")
+    monkeypatch.setenv("FUSCO_PUSH_ROUNDS", "1")
+    pkg, topo, pl, a, tb, payload = _cluster_case(P, E, K, T_l, hidden, "bf16", 0.5, seed=77 + P)
+    res = _run_cluster(pkg, topo, pl, a, tb, payload, "bf16", "f64")
+    layouts, row_of = _check_layout(res, a, pl, P)
+    acts = O.dispatch(payload, layouts)
+    for g in range(P):
+        assert np.array_equal(res["acts"][g], acts[g]), f"activation/{g}"
+    for s in range(P):
+        want = O.combine(acts, row_of, a.experts, a.weights, pl.owner, res["ids"][s], "bf16")
+        assert np.array_equal(res["outs"][s], want), f"output/{s}"
+
+
 def test_engine_parity_fp32_payload(engines):
     """fp32 rows (the reference's own payload dtype) through both engines."""
     pkg, topo, pl, a, tb, payload = _cluster_case(4, 32, 4, 300, 1024, "f32", 0.7, seed=9)

@@ -52,6 +52,19 @@ def main():
     for ctas in (148 * 4, 148 * 8):
         out[f"fs_probe_fill_{ctas}_gbs"] = best(
             lambda: _lib.check(lib.fs_probe_copy(0, c_void_p(b.data_ptr()), c_void_p(0), n, ctas, st)), n)
+    # the P=1 dispatch's pattern: 4096 rows of 14336 B, each written to 8 of
+    # 32768 destination rows in a random order (read 59 MB, write 470 MB)
+    rows, fan, rb = 4096, 8, 14336
+    src = torch.empty(rows * rb, dtype=torch.uint8, device="cuda").fill_(1)
+    dst = torch.empty(rows * fan * rb, dtype=torch.uint8, device="cuda")
+    perm = torch.randperm(rows * fan, device="cuda").to(torch.int32)
+    for ctas in (148 * 3, 148 * 6):
+        for ro in (0, 1):
+            out[f"fs_probe_scatter_{'w' if ro else 'rw'}_{ctas}_gbs"] = best(
+                lambda: _lib.check(lib.fs_probe_scatter(0, c_void_p(dst.data_ptr()),
+                                                        c_void_p(0 if ro else src.data_ptr()),
+                                                        c_void_p(perm.data_ptr()), rows, fan, rb, ctas, st)),
+                rows * fan * rb + (0 if ro else rows * rb))
     print(json.dumps({k: round(v, 1) for k, v in out.items()}))
 
 
