@@ -59,6 +59,50 @@ NVLINK_NOMINAL = 900.0   # GB/s per direction per GPU (NVLink 5)
 NVLINK_MEASURED = 770.0  # GB/s peer copy, B200_PROFILING.md
 
 
+def pattern_ceiling(T: int, K: int, tb: int, dev) -> float | None:
+    """HBM GB/s of the P=1 dispatch's access pattern without its metadata:
+    T rows read once, each written to K of T*K rows in a random order
+    (fs_probe_scatter).  Scattered 14 KB row writes do not reach the
+    sequential copy peak; this is the ceiling the dispatch is judged against
+    beside the MEASURED_PEAKS copy figure."""
+    try:
+        from ctypes import c_void_p
+
+        import torch
+
+        from paper_2512_22036_b200 import _lib
+
+        if tb % 16:
+            return None
+        lib = _lib.load()
+        src = torch.empty(T * tb, dtype=torch.uint8, device=dev).fill_(1)
+        dst = torch.empty(T * K * tb, dtype=torch.uint8, device=dev)
+        perm = torch.randperm(T * K, device=dev).to(torch.int32)
+        st = c_void_p(torch.cuda.current_stream().cuda_stream)
+        nbytes = T * tb + T * K * tb
+        best = 0.0
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        for ctas in (3 * sms, 6 * sms):
+            run = lambda: _lib.check(lib.fs_probe_scatter(dev.index or 0, c_void_p(dst.data_ptr()),
+                                                          c_void_p(src.data_ptr()), c_void_p(perm.data_ptr()),
+                                                          T, K, tb, ctas, st))
+            run()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ts = []
+            for _ in range(10):
+                ev[0].record()
+                run()
+                ev[1].record()
+                ev[1].synchronize()
+                ts.append(ev[0].elapsed_time(ev[1]) * 1e-3)
+            best = max(best, nbytes / min(ts) / 1e9)
+        del src, dst, perm
+        torch.cuda.empty_cache()
+        return best
+    except Exception:  # informational only: never fails the bench line
+        return None
+
+
 def peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -585,6 +629,13 @@ def main() -> int:
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk["hbm"], "unit": "GB/s",
                 "frac": achieved / pk["hbm"], "peak_src": pk["hbm_src"], "bytes_per_launch": b,
                 "traffic": None}
+        if dom == "fs_dispatch":
+            pc = pattern_ceiling(T_l, K, tb, dev)
+            if pc:
+                roof["pattern_ceiling"] = {"value": pc, "unit": "GB/s", "frac": achieved / pc,
+                                           "src": "fs_probe_scatter in-run: the same rows read once and written "
+                                                  "to K scattered rows with plain 16-byte stores, no metadata "
+                                                  "(best of 2 grids, 10 reps)"}
     else:
         # bottleneck rank's NVLink bytes (max of egress / ingress over ranks);
         # the kernel floor is the slower of that over the link and its HBM bytes

@@ -22,9 +22,12 @@ namespace cg = cooperative_groups;
 // cannot start before every peer published its next-epoch counts, i.e.
 // finished pulling this epoch's rows in combine (fusco.cu region_layout).
 // ===========================================================================
+#ifndef FUSCO_MOVE_U
+#define FUSCO_MOVE_U 8  // 16-byte words per lane per dispatch unit (A/B builds)
+#endif
 template <typename V>
 struct MoveCfg {
-  static constexpr int U = sizeof(V) == 16 ? 8 : 16;  // words per lane per unit (4 KB / 2 KB)
+  static constexpr int U = sizeof(V) == 16 ? FUSCO_MOVE_U : 16;  // words per lane per unit (4 KB / 2 KB)
   static constexpr int kSliceWords = 32 * U;
 };
 

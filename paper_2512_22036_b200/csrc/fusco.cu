@@ -710,7 +710,7 @@ int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_byte
   // Grid sized to the work: every CTA joins the end-of-push count (one
   // acq_rel atomic each), so idle CTAs only add latency at decode sizes.
   // At least one CTA per SM (the receiver fan-out uses the same grid).
-  const int U = vec16 ? 8 : 16, elem = vec16 ? 16 : 4;
+  const int U = vec16 ? MoveCfg<int4>::U : MoveCfg<int>::U, elem = vec16 ? 16 : 4;
   const long long slices = ((long long)h->tb / elem + 32 * U - 1) / (32 * U);
   const long long units = (long long)num_tokens * slices;
   const long long want = (units + kMoveThreads / 32 - 1) / (kMoveThreads / 32);
