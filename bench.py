@@ -411,11 +411,13 @@ def main() -> int:
     P_ = lambda t: c_void_p(t.data_ptr())  # noqa: E731
     lay_args = (h, P_(idx), idx.element_size(), T_l, P_(plan.row_of), P_(plan.expert_counts),
                 P_(plan.expert_offsets), None, None, P_(plan.stats), FS_PHASE_ALL, stream)
-    disp_args = [(h, P_(xs[j]), P_(idx), idx.element_size(), P_(plan.row_of), T_l, FS_PHASE_ALL, stream)
+    # dispatch with the router weights: owners pre-reduce a token's groups of
+    # >= 3 rows for the fp32-accumulate combine (P > 1; FUSCO_OWNER_REDUCE=0 off)
+    disp_args = [(h, P_(xs[j]), P_(idx), idx.element_size(), P_(plan.row_of), P_(w), 4, T_l, FS_PHASE_ALL, stream)
                  for j in range(NSET)]
     comb_args = [(h, P_(idx), idx.element_size(), P_(plan.row_of), P_(w), 4, T_l, P_(outs[j]), buf.dtype_code,
                   FS_SRC_ACT, 0, FS_PHASE_ALL, stream) for j in range(NSET)]
-    f_layout, f_disp, f_comb = lib.fs_layout, lib.fs_dispatch, lib.fs_combine
+    f_layout, f_disp, f_comb = lib.fs_layout, lib.fs_dispatch_w, lib.fs_combine
 
     def step(j, ev=None):
         if ev is not None:
@@ -573,7 +575,7 @@ def main() -> int:
             s_cmp.wait_event(ev_in[q])
             s_cmp.wait_event(ev_out[q])
             p = buf.build_plan(idx_d[q], stream=s_cmp)
-            buf.dispatch(xd[q], p, stream=s_cmp)
+            buf.dispatch(xd[q], p, stream=s_cmp, topk_w=w_d[q])
             buf.combine(p, w_d[q], out=od[q], src="act", stream=s_cmp)
             ev_used[q].record(s_cmp)
             ev_done[q].record(s_cmp)
@@ -714,6 +716,8 @@ def main() -> int:
         "launch_mode": "cuda_graph" if graph is not None else "eager",
         "dispatch_engine": args.dispatch if args.dispatch != "auto" else ("tma" if P == 1 else "warp"),
         "combine_engine": args.combine if args.combine != "auto" else ("warp" if P == 1 else "tma"),
+        "owner_reduce": bool(P > 1 and 2 <= K <= 8 and os.environ.get("FUSCO_OWNER_REDUCE", "1") != "0"
+                             and (args.combine in ("auto", "tma"))),
         "host_enqueue_ms_per_step": host_ms / args.steps,
         "clocks": clocks,
     }

@@ -189,6 +189,17 @@ int fs_layout(fs_handle_t h, const void* topk_idx, int idx_bytes, int num_tokens
 int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_bytes,
                 const int32_t* row_of, int num_tokens, int phase, void* stream);
 
+/* fs_dispatch with the router weights topk_w[num_tokens, topk] (fp32 if
+ * w_bytes==4, f64 if 8; the same array the combine gets).  With weights the
+ * dispatch also describes, for each token with several experts on one remote
+ * owner, that group to the owner, and a combine of this step with fp32
+ * accumulation lets the owner pre-reduce the group (one fp32 partial per
+ * (token, owner) pulled instead of its rows; see fs_combine).  topk_w NULL
+ * is fs_dispatch.  Replaces the same reference calls as fs_dispatch. */
+int fs_dispatch_w(fs_handle_t h, const void* x, const void* topk_idx, int idx_bytes,
+                  const int32_t* row_of, const void* topk_w, int w_bytes, int num_tokens,
+                  int phase, void* stream);
+
 /* Combine: out[t] = Σ_{k ascending} w[t,k] · src_owner(t,k)[row_of[t,k]],
  * pulled from the peers' act / act_out rows.  topk_w is f32 (w_bytes 4) or
  * f64 (w_bytes 8); out has the payload dtype. */

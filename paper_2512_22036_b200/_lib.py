@@ -57,6 +57,7 @@ SIGNATURES = {
          c_int, c_void_p],
     ),
     "fs_dispatch": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int, c_int, c_void_p]),
+    "fs_dispatch_w": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p]),
     "fs_combine": (
         c_int,
         [c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_int,

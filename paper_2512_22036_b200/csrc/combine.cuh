@@ -335,6 +335,86 @@ __global__ void __launch_bounds__(kMoveThreads)
 }
 
 // ===========================================================================
+// Owner-side pre-reduction (combine LOCAL phase, a.reduce): for every record a
+// source wrote into this rank's region this epoch (dispatch_kernel) with at
+// least mmin rows here, the partial Σ_{k in group, ascending} w_k · y[row_k]
+// in fp32 goes to the partial slot [source][token] of this rank's region
+// (2·tb bytes: fp32 of the hidden dim).  Every warp of the grid takes
+// (source, token) slots in turn; lanes stride the 16-byte column chunks.
+// ===========================================================================
+template <bool BF16>
+__device__ void owner_prereduce(const FsArgs& a, uint32_t epoch, size_t src_off, int mmin) {
+  using EL = Elem<int4, BF16>;
+  const int P = a.world, s = a.rank, K = a.K, tb = a.tb, nv = tb / 16;
+  const int lane = threadIdx.x & 31;
+  const int par = (int)(epoch & 1u);
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const char* src = a.peer[s] + src_off;
+  const GrpRec* recs = reinterpret_cast<const GrpRec*>(a.peer[s] + a.off_grp);
+  char* part = a.peer[s] + a.off_part;
+  const long long slots = (long long)P * a.max_tokens;
+  int q_cached = -1, tq = 0;
+  for (long long it = gw; it < slots; it += nw) {
+    const int q = (int)(it / a.max_tokens), t = (int)(it - (long long)q * a.max_tokens);
+    if (q == s) continue;
+    if (q != q_cached) {  // the source's token count this epoch (its count word, complete since the planner)
+      tq = read_count_word(a, par, epoch, q, a.E);
+      q_cached = q;
+    }
+    if (t >= tq) continue;
+    const GrpRec* rec = recs + it;
+    const uint32_t e = __ldcg(&rec->epoch), km = __ldcg(&rec->kmask);
+    if (e != epoch || __popc(km) < mmin) continue;
+    int rk = 0;
+    float wk = 0.f;
+    if (lane < K && ((km >> lane) & 1u)) {
+      rk = __ldcg(&rec->rows[lane]);
+      wk = __ldcg(&rec->w[lane]);
+      if (rk < 0 || rk >= a.max_rows) {
+        record_error(a.status, FS_ERANGE, kSiteRows);
+        rk = 0;
+      }
+    }
+    int rr[kGrpMaxK];
+    float ww[kGrpMaxK];
+#pragma unroll
+    for (int k = 0; k < kGrpMaxK; ++k) {  // every lane takes part (before the column loop)
+      rr[k] = __shfl_sync(kFull, rk, k);
+      ww[k] = __shfl_sync(kFull, wk, k);
+    }
+    char* dst = part + (size_t)it * 2 * tb;
+    for (int v = lane; v < nv; v += 32) {
+      float acc[EL::N];
+#pragma unroll
+      for (int e2 = 0; e2 < EL::N; ++e2) acc[e2] = 0.f;
+#pragma unroll
+      for (int k0 = 0; k0 < kGrpMaxK; k0 += 4) {  // four rows' loads in flight, k ascending
+        int4 x[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k = k0 + j;
+          if (k < K && ((km >> k) & 1u)) x[j] = ld_nc(reinterpret_cast<const int4*>(src + (size_t)rr[k] * tb) + v);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k = k0 + j;
+          if (k < K && ((km >> k) & 1u)) {
+#pragma unroll
+            for (int e2 = 0; e2 < EL::N; ++e2) acc[e2] = __fmaf_rn(ww[k], EL::get(x[j], e2), acc[e2]);
+          }
+        }
+      }
+      int4* o = reinterpret_cast<int4*>(dst) + (size_t)v * (EL::N / 4);
+#pragma unroll
+      for (int h = 0; h < EL::N / 4; ++h)
+        st_na(o + h, make_int4(__float_as_int(acc[4 * h]), __float_as_int(acc[4 * h + 1]),
+                               __float_as_int(acc[4 * h + 2]), __float_as_int(acc[4 * h + 3])));
+    }
+  }
+}
+
+// ===========================================================================
 // Combine, TMA engine
 //
 // Work item = (token i, column slice j of SB bytes).  Warp 0 resolves the
@@ -360,7 +440,7 @@ __host__ __device__ inline int comb_slice_bytes(int tb, int K, int stage_target 
 }
 
 template <bool BF16, bool ACC64>
-__global__ void __launch_bounds__(kCombThreads)
+__global__ void __launch_bounds__(kCombThreads, 3)  // 3 CTAs/SM (the stage budget assumes it)
     combine_tma_kernel(FsArgs a, const void* __restrict__ idx, const int32_t* __restrict__ row_of,
                        const void* __restrict__ topk_w, int w64, char* __restrict__ out, int src_sel,
                        int phase, int nstages, int sb) {
@@ -372,6 +452,8 @@ __global__ void __launch_bounds__(kCombThreads)
   // by the producer before it arms the stage's full barrier
   __shared__ long long slot_item[kCombMaxStages];
   __shared__ Acc slot_w[kCombMaxStages][32];
+  __shared__ int8_t slot_kind[kCombMaxStages][32];  // per stage and lane: 0 row, 1/2 partial halves, 3 none
+  __shared__ int8_t slot_k2[kCombMaxStages][32];    // lane holding the partial's second half (bf16)
   __shared__ int32_t owner_cmb[kMaxExperts];
   uint64_t* full = reinterpret_cast<uint64_t*>(csm);
   uint64_t* empty = full + kCombMaxStages;
@@ -397,13 +479,31 @@ __global__ void __launch_bounds__(kCombThreads)
       src_sel == FS_SRC_ACT_OUT ? a.off_actout : a.off_act;
   trace_stamp(a, FS_TRACE_COMBINE_BEGIN);
 
+  // owner-side pre-reduction (fp32 accumulate only; bf16 rows: groups of >= 3,
+  // whose fp32 partial is smaller than the rows; fp32 rows: groups of >= 2)
+  const bool red = !ACC64 && a.reduce && P > 1;
+  const int mmin = BF16 ? 3 : 2;
   if ((phase & FS_PHASE_LOCAL) && P > 1) {
-    if (blockIdx.x == 0 && threadIdx.x < P)
+    if (red) {
+      owner_prereduce<BF16>(a, epoch, src_off, mmin);
+      cg::this_grid().sync();  // every partial written before the "ready" release below
+    }
+    if (blockIdx.x == 0 && threadIdx.x < P) {
+      if (red) reinterpret_cast<volatile uint32_t*>(a.peer[threadIdx.x] + kOffModeFlag)[s] = epoch;
       st_release_sys_u32(reinterpret_cast<uint32_t*>(a.peer[threadIdx.x] + kOffReadyFlag) + s, epoch);
+    }
   }
   if (!remote) return;
-  if (P > 1 && threadIdx.x < P)
+  __shared__ uint32_t red_mask;  // owners whose partials this CTA pulls (this epoch)
+  if (threadIdx.x == 0) red_mask = 0u;
+  __syncthreads();
+  if (P > 1 && threadIdx.x < P) {
     wait_u32_geq(reinterpret_cast<const uint32_t*>(a.peer[s] + kOffReadyFlag) + threadIdx.x, epoch, a);
+    // the owner's mode word precedes its ready release: read after the acquire
+    if (red && threadIdx.x != s &&
+        reinterpret_cast<volatile const uint32_t*>(a.peer[s] + kOffModeFlag)[threadIdx.x] == epoch)
+      atomicOr(&red_mask, 1u << threadIdx.x);
+  }
   __syncthreads();
   // the rows the bulk copies (async proxy) read were published to generic-proxy acquires
   if (P > 1 && threadIdx.x < 32) fence_proxy_async_global();
@@ -451,13 +551,39 @@ __global__ void __launch_bounds__(kCombThreads)
         r = (m.r < 0 || m.r >= a.max_rows) ? 0 : m.r;
         slot_w[q][lane] = wl;
       }
+      // Source side of the pre-reduction: a group of >= mmin of the token's
+      // rows on an owner that pre-reduced is one fp32 partial slice (2·len
+      // bytes for bf16, loaded as two halves into the slots of the group's
+      // first two lanes); its other lanes load nothing.  kind: 0 row,
+      // 1 partial (first half), 2 partial second half, 3 skipped.
+      int kind = 0, second = 0;
+      if (red_mask) {
+        const uint32_t same = __match_any_sync(kFull, lane < K ? g : -1 - lane);
+        const bool grp = lane < K && ((red_mask >> g) & 1u) && __popc(same) >= mmin;
+        const int first = __ffs(same) - 1;
+        second = __ffs(same & ~(1u << first)) - 1;
+        kind = !grp ? 0 : (lane == first ? 1 : ((BF16 && lane == second) ? 2 : 3));
+      }
+      if (lane < K) {
+        slot_kind[q][lane] = (int8_t)kind;
+        slot_k2[q][lane] = (int8_t)second;
+      }
       if (lane == 0) slot_item[q] = u;
+      const uint32_t nb = (lane < K && kind != 3) ? (uint32_t)len : 0u;
+      const uint32_t tx = __reduce_add_sync(kFull, nb);
       __syncwarp();
-      if (lane == 0) mbar_arrive_expect_tx(&full[q], (uint32_t)(K * len));
+      if (lane == 0) mbar_arrive_expect_tx(&full[q], tx);
       __syncwarp();
-      if (lane < K)
-        bulk_load(stages + (size_t)q * stage_bytes + (size_t)lane * sb,
-                  a.peer[g] + src_off + (size_t)r * tb + off, (uint32_t)len, &full[q]);
+      if (lane < K) {
+        char* dstage = stages + (size_t)q * stage_bytes + (size_t)lane * sb;
+        if (kind == 0) {
+          bulk_load(dstage, a.peer[g] + src_off + (size_t)r * tb + off, (uint32_t)len, &full[q]);
+        } else if (kind != 3) {
+          const int i = (int)((uint32_t)u / (uint32_t)S);
+          const char* pp = a.peer[g] + a.off_part + ((size_t)s * a.max_tokens + i) * 2 * tb + (BF16 ? 2 * off : off);
+          bulk_load(dstage, pp + (kind == 2 ? len : 0), (uint32_t)len, &full[q]);
+        }
+      }
       u = un;
       m = mn;
       wl = wn;
@@ -478,10 +604,26 @@ __global__ void __launch_bounds__(kCombThreads)
 #pragma unroll
         for (int e = 0; e < EL::N; ++e) acc[e] = (Acc)0;
         for (int k = 0; k < K; ++k) {
-          const Acc wk = slot_w[q][k];
-          const int4 x = *reinterpret_cast<const int4*>(st + (size_t)k * sb + (size_t)v * 16);
+          const int kd = slot_kind[q][k];
+          if (kd == 0) {
+            const Acc wk = slot_w[q][k];
+            const int4 x = *reinterpret_cast<const int4*>(st + (size_t)k * sb + (size_t)v * 16);
 #pragma unroll
-          for (int e = 0; e < EL::N; ++e) acc[e] = fma_acc<Acc>(wk, EL::get(x, e), acc[e]);
+            for (int e = 0; e < EL::N; ++e) acc[e] = fma_acc<Acc>(wk, EL::get(x, e), acc[e]);
+          } else if (kd == 1) {  // fp32 partial of the owner's group, already weighted
+            const int len = nv * 16;
+            const int k2 = slot_k2[q][k];
+#pragma unroll
+            for (int h = 0; h < EL::N / 4; ++h) {
+              const int pb = v * EL::N * 4 + h * 16;  // byte offset in the slice's fp32 partial
+              const char* src = pb < len ? st + (size_t)k * sb + pb : st + (size_t)k2 * sb + (pb - len);
+              const int4 f = *reinterpret_cast<const int4*>(src);
+              acc[4 * h] += (Acc)__int_as_float(f.x);
+              acc[4 * h + 1] += (Acc)__int_as_float(f.y);
+              acc[4 * h + 2] += (Acc)__int_as_float(f.z);
+              acc[4 * h + 3] += (Acc)__int_as_float(f.w);
+            }
+          }
         }
         int4 o;
 #pragma unroll

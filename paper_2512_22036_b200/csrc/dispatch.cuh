@@ -391,6 +391,20 @@ __global__ void __launch_bounds__(kMoveThreads, FUSCO_DISP_MINB)
     // receiver's fan-out instead of crossing the link again
     if (P > 1 && sl == 0 && lane < K && r >= 0 && !direct && r_first >= 0)
       list_duplicate(a, epoch, g, b, r, r_first);
+    // pre-reduction record for the owner of >= 2 of the token's rows (the
+    // combine decides whether the group is large enough to pre-reduce); plain
+    // stores, published with the unit's block like the rows themselves
+    if (a.disp_w != nullptr && sl == 0 && lane < K && g != s && __popc(same) >= 2) {
+      GrpRec* rec = reinterpret_cast<GrpRec*>(a.peer[g] + a.off_grp) + (size_t)s * a.max_tokens + i;
+      const size_t wi = (size_t)i * K + lane;
+      rec->rows[lane] = r;
+      rec->w[lane] = a.disp_w64 ? (float)reinterpret_cast<const double*>(a.disp_w)[wi]
+                                : reinterpret_cast<const float*>(a.disp_w)[wi];
+      if (lane == first_lane) {
+        rec->kmask = same;
+        rec->epoch = epoch;
+      }
+    }
     // Rotate the destination order by token so concurrent warps of this
     // rank spread their first stores over different peers.
     const int rot = a.balance ? (i + s) % K : 0;

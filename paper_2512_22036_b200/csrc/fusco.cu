@@ -38,11 +38,21 @@ struct RegionLayout {
   size_t off_count, count_stride, off_blkflag, off_dupq, off_act, act_stride, off_actout, total;
   int blk, nbmax;
   long long dupq_cap;
+  size_t off_grp, off_part;  // owner-side pre-reduction (0: not configured)
 };
 
 int blocks_per_source(int max_tokens) {
   const int blk = block_tokens(max_tokens);
   return std::max(1, (max_tokens + blk - 1) / blk);
+}
+
+// Owner-side pre-reduction buffers are part of the region when P > 1 and
+// 2 <= K <= 8, unless FUSCO_OWNER_REDUCE=0 (read identically by
+// fs_region_bytes and fs_create, so every rank sizes its region the same).
+bool owner_reduce_configured(int world, int K) {
+  const char* e = getenv("FUSCO_OWNER_REDUCE");
+  if (e && std::string(e) == "0") return false;
+  return world > 1 && K >= 2 && K <= kGrpMaxK;
 }
 
 RegionLayout region_layout(int world, int E, int K, int tb, int max_tokens, long long max_rows, int with_act_out) {
@@ -62,6 +72,12 @@ RegionLayout region_layout(int world, int E, int K, int tb, int max_tokens, long
   // rank has published the next epoch's counts, i.e. finished this combine
   L.off_actout = L.off_act + L.act_stride;
   L.total = L.off_actout + (with_act_out ? L.act_stride : 0);
+  L.off_grp = L.off_part = 0;
+  if (owner_reduce_configured(world, K)) {
+    L.off_grp = align256(L.total);
+    L.off_part = L.off_grp + align256((size_t)world * std::max(max_tokens, 0) * sizeof(GrpRec));
+    L.total = L.off_part + (size_t)world * std::max(max_tokens, 0) * 2 * (size_t)tb;
+  }
   return L;
 }
 
@@ -110,6 +126,8 @@ struct fs_ctx {
   uint32_t* jorder_d;              // [P * nbmax]
   int push_warps;                  // warps per dispatch CTA that push before fanning out
   int claim_tokens;                // dispatch claim granularity: 1 = whole tokens, 0 = (token, slice) units
+  int recs_written;                // this epoch's dispatch wrote pre-reduction records (fs_dispatch_w)
+  int owner_reduce_off;            // FUSCO_OWNER_REDUCE=0 at combine time (A/B)
   int push_rounds;                 // FUSCO_PUSH_ROUNDS=1: per-CTA-round completion counts (A/B; default per unit)
   int fan_split;                   // FUSCO_FAN_SPLIT: -1 auto (by batch size), 0 rows, 1 slices
   int fan_poll;                    // FUSCO_FAN_POLL: 1 = per-CTA cached fan-out polling
@@ -147,6 +165,9 @@ FsArgs make_args(const fs_ctx* h, int T, int idx64) {
   a.count_stride = h->L.count_stride;
   a.act_stride = h->L.act_stride;
   a.blk = h->L.blk;
+  a.off_grp = h->L.off_grp;
+  a.off_part = h->L.off_part;
+  a.max_tokens = h->max_tokens;
   a.nbmax = h->L.nbmax;
   a.dupq_cap = h->L.dupq_cap;
   a.push_warps = h->push_warps;
@@ -428,6 +449,8 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
     h->claim_tokens = cl && std::string(cl) == "token";
     const char* db = getenv("FUSCO_DBG_BLK");
     h->dbg_relaxed = db && std::string(db) == "1";
+    h->recs_written = 0;
+    h->owner_reduce_off = !h->L.off_grp;
     const char* pr = getenv("FUSCO_PUSH_ROUNDS");
     h->push_rounds = pr && std::string(pr) == "1";
     const char* fsp = getenv("FUSCO_FAN_SPLIT");
@@ -645,7 +668,13 @@ int fs_layout(fs_handle_t h, const void* topk_idx, int idx_bytes, int num_tokens
 
 int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_bytes, const int32_t* row_of,
                 int num_tokens, int phase, void* stream) {
+  return fs_dispatch_w(h, x, topk_idx, idx_bytes, row_of, nullptr, 4, num_tokens, phase, stream);
+}
+
+int fs_dispatch_w(fs_handle_t h, const void* x, const void* topk_idx, int idx_bytes, const int32_t* row_of,
+                  const void* topk_w, int w_bytes, int num_tokens, int phase, void* stream) {
   if (!h) return fail(FS_EINVAL, "null handle");
+  if (topk_w && w_bytes != 4 && w_bytes != 8) return fail(FS_EINVAL, "w_bytes must be 4 or 8");
   FS_CUDA(cudaSetDevice(h->device));
   if (int rc = check_idx_bytes(idx_bytes)) return rc;
   if (num_tokens < 0 || num_tokens > h->max_tokens)
@@ -658,6 +687,15 @@ int fs_dispatch(fs_handle_t h, const void* x, const void* topk_idx, int idx_byte
   if (h->disp_phases & phase) return fail(FS_EINVAL, "fs_dispatch already ran for this plan: call fs_layout first");
   h->disp_phases |= phase;
   FsArgs a = make_args(h, num_tokens, idx_bytes == 8);
+  // owner-side pre-reduction records (warp engine, P > 1, weights given): the
+  // combine of this epoch may then pull fp32 partials for them
+  const bool vec16_x = (h->tb % 16 == 0) && aligned(x, 16);
+  const bool recs = topk_w && h->L.off_grp && h->world > 1 && !(h->dispatch_tma && vec16_x);
+  if (phase & FS_PHASE_LOCAL) h->recs_written = recs ? 1 : 0;
+  if (recs) {
+    a.disp_w = topk_w;
+    a.disp_w64 = w_bytes == 8;
+  }
   // receiver fan-out unit: a row slice at small batches (few duplicate rows:
   // spread them over every warp), a whole row otherwise (FUSCO_FAN_SPLIT=0|1 overrides)
   a.fan_split = h->fan_split >= 0 ? h->fan_split : (num_tokens <= kFanSplitTokens ? 1 : 0);
@@ -753,6 +791,9 @@ int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes, const int32_t
   void* args[] = {&a, (void*)&topk_idx, (void*)&row_of, (void*)&topk_w, &w64, &out, &src, &phase};
   const void* fn;
   const bool bf = dtype == FS_DTYPE_BF16, f64 = acc == FS_ACC_F64;
+  // owner-side pre-reduction: this epoch's dispatch wrote the records
+  // (fs_dispatch_w), fp32 accumulation, the TMA engine (P > 1 default)
+  a.reduce = (h->combine_tma && vec16 && !f64 && h->world > 1 && h->recs_written && !h->owner_reduce_off) ? 1 : 0;
   if (h->combine_tma && vec16) {
     fn = bf ? (f64 ? (const void*)combine_tma_kernel<true, true> : (const void*)combine_tma_kernel<true, false>)
             : (f64 ? (const void*)combine_tma_kernel<false, true> : (const void*)combine_tma_kernel<false, false>);

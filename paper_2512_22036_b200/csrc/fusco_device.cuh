@@ -26,6 +26,23 @@ constexpr int kMoveThreads = 256;  // dispatch / combine warp-mover CTA size
 constexpr size_t kSigBytes = 4096;
 constexpr size_t kOffCountFlag = 0;    // u32[FS_MAX_RANKS]: reserved (the counts are epoch-tagged words)
 constexpr size_t kOffReadyFlag = 256;  // u32[FS_MAX_RANKS]: expert outputs ready
+constexpr size_t kOffModeFlag = 512;   // u32[FS_MAX_RANKS]: owner g pre-reduced this epoch (= epoch)
+
+// Owner-side pre-reduction (combine, fp32 accumulate, P > 1): for a token
+// with m >= 3 (bf16 rows; m >= 2 for fp32 rows) of its K experts on one
+// remote owner, the owner sums w_k * y_k over those rows in fp32 (k
+// ascending) and the source pulls that one fp32 partial instead of the m
+// rows.  The source describes each such (token, owner) group during the
+// dispatch: a record in the owner's region, slot [source][token].
+constexpr int kGrpMaxK = 8;
+struct GrpRec {
+  uint32_t epoch;
+  uint32_t kmask;  // the token's k's owned by this rank
+  int32_t rows[kGrpMaxK];
+  float w[kGrpMaxK];
+  uint32_t pad[2];
+};
+static_assert(sizeof(GrpRec) == 80, "GrpRec layout");
 
 // Completion blocks of the dispatch (P > 1): a source's tokens are cut into
 // blocks of FsArgs::blk tokens; when every unit of block b has been pushed, the
@@ -73,6 +90,12 @@ struct FsArgs {
   int push_warps;            // warps per CTA that push first (the rest fan out from the start)
   int claim_tokens;          // 1: pushers claim whole tokens (all slices), 0: (token, slice) units
   int dbg_relaxed;           // timing experiments only: block counts without release ordering
+  // owner-side pre-reduction (0 in every field when the handle has no partial buffers)
+  size_t off_grp, off_part;  // region offsets: GrpRec[P][max_tokens], fp32 partials [P][max_tokens][2 * tb]
+  int max_tokens;
+  const void* disp_w;        // fs_dispatch_w: the router weights [T, K] (records are written when set)
+  int disp_w64;
+  int reduce;                // combine: pre-reduce as owner and pull partials as source (this epoch)
   int push_rounds;           // 1: completion counted per CTA round (FUSCO_PUSH_ROUNDS=1), 0: per unit (default)
   int fan_split;             // 1: fan-out units are row slices (small batches), 0: whole rows
   int fan_poll;              // 1: fan-out waits poll through a per-CTA shared-memory cache (FUSCO_FAN_POLL)

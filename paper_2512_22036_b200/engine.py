@@ -240,16 +240,29 @@ class Rank:
         plan.epoch = self.epoch
         return plan
 
-    def dispatch(self, x: torch.Tensor, plan: Plan, phase: int = FS_PHASE_ALL, stream=None) -> None:
+    def dispatch(self, x: torch.Tensor, plan: Plan, phase: int = FS_PHASE_ALL, stream=None,
+                 topk_w: torch.Tensor | None = None) -> None:
+        """fs_dispatch, or fs_dispatch_w when the router weights are given (the
+        owners may then pre-reduce groups of a token's rows for an fp32-
+        accumulate combine of this step; include/fusco.h)."""
         if x.shape[0] != plan.num_tokens or x.numel() * x.element_size() != plan.num_tokens * self.token_bytes:
             raise ValueError("x must be [T, token_bytes] bytes matching the plan")
         if not x.is_contiguous() or x.device != self.device:
             raise ValueError("x must be contiguous on the rank's device")
         if plan.epoch != self.epoch:
             raise ValueError("plan is stale: build a new plan (fs_layout) before dispatch")
+        if topk_w is None:
+            call(
+                "fs_dispatch", self.handle, ptr(x), ptr(plan.topk_idx), plan.topk_idx.element_size(),
+                ptr(plan.row_of), plan.num_tokens, phase, self._stream(stream),
+            )
+            return
+        if (topk_w.shape != plan.topk_idx.shape or topk_w.dtype not in (torch.float32, torch.float64)
+                or not topk_w.is_contiguous() or topk_w.device != self.device):
+            raise ValueError("topk_w must be a contiguous f32/f64 [T, K] tensor on the rank's device")
         call(
-            "fs_dispatch", self.handle, ptr(x), ptr(plan.topk_idx), plan.topk_idx.element_size(),
-            ptr(plan.row_of), plan.num_tokens, phase, self._stream(stream),
+            "fs_dispatch_w", self.handle, ptr(x), ptr(plan.topk_idx), plan.topk_idx.element_size(),
+            ptr(plan.row_of), ptr(topk_w), topk_w.element_size(), plan.num_tokens, phase, self._stream(stream),
         )
 
     def combine(
@@ -414,10 +427,10 @@ class EmulatedCluster:
             self._phase_done()
         return plans
 
-    def dispatch(self, xs: list[torch.Tensor], plans: list[Plan]) -> None:
+    def dispatch(self, xs: list[torch.Tensor], plans: list[Plan], ws: list[torch.Tensor] | None = None) -> None:
         for ph in self._phases():
-            for r, x, p in zip(self.ranks, xs, plans):
-                r.dispatch(x, p, ph)
+            for j, (r, x, p) in enumerate(zip(self.ranks, xs, plans)):
+                r.dispatch(x, p, ph, topk_w=None if ws is None else ws[j])
             self._phase_done()
 
     def combine(self, plans, ws, outs, *, dtype_code: int, src: int = FS_SRC_ACT, acc: int = FS_ACC_F32):
@@ -524,12 +537,16 @@ class EPBuffer:
         plan = self.r.new_plan(topk_idx, with_masks)
         return self.r.layout(plan, FS_PHASE_ALL, stream)
 
-    def dispatch(self, x: torch.Tensor, plan: Plan, stream=None, rows: int | None = None) -> torch.Tensor:
+    def dispatch(self, x: torch.Tensor, plan: Plan, stream=None, rows: int | None = None,
+                 topk_w: torch.Tensor | None = None) -> torch.Tensor:
         """Returns this rank's activation view [rows, hidden] (rows = max_rows
-        unless given; the valid prefix is plan.expert_offsets[-1])."""
+        unless given; the valid prefix is plan.expert_offsets[-1]).  With the
+        router weights (the ones the combine will get), an fp32-accumulate
+        combine of this step lets each owner pre-reduce groups of >= 3 of a
+        token's rows (>= 2 for fp32 rows) into one fp32 partial."""
         if x.dtype != self.dtype or x.dim() != 2 or x.shape[1] != self.hidden:
             raise ValueError(f"x must be [T, {self.hidden}] {self.dtype}")
-        self.r.dispatch(x, plan, FS_PHASE_ALL, stream)
+        self.r.dispatch(x, plan, FS_PHASE_ALL, stream, topk_w=topk_w)
         return self.r.act(rows, self.dtype)
 
     execute_dispatch = dispatch

@@ -54,6 +54,15 @@ def main() -> int:
         else:
             out = buf.combine(plan, w, src="act", acc="f64")
         buf.check()
+        # the same shuffle with the router weights at dispatch and fp32
+        # accumulation: the owners pre-reduce groups of a token's rows
+        # (production P > 1 path), within the stated tolerance
+        w32 = w.float().contiguous()
+        plan32 = buf.build_plan(idx)
+        act32 = buf.dispatch(x, plan32, topk_w=w32)
+        out32 = buf.combine(plan32, w32, src="act", acc="f32")
+        buf.check()
+        tol = dict(rtol=2.0**-8, atol=1e-3) if dt == "bf16" else dict(rtol=1e-5, atol=1e-6)
         layouts, row_of = O.activation_layouts(a.experts, a.source, pl.owner, P)
         if not np.array_equal(plan.row_of.cpu().numpy(), row_of[ids]):
             print(f"[rank {rank}] iter {it}: row_of mismatch", flush=True)
@@ -73,6 +82,10 @@ def main() -> int:
             if not np.array_equal(got, want):
                 print(f"[rank {rank}] iter {it}: output mismatch", flush=True)
                 failures += 1
+            got32 = out32.view(torch.uint8).reshape(ids.size, -1)[torch.as_tensor(loc, device=dev)].cpu().numpy()
+            if not np.allclose(O.decode(got32, dt), O.decode(want, dt), **tol):
+                print(f"[rank {rank}] iter {it}: fp32 (owner pre-reduced) output out of tolerance", flush=True)
+                failures += 1
             del pay_d
             continue
         acts = O.dispatch(payload, layouts)
@@ -84,6 +97,9 @@ def main() -> int:
         if not np.array_equal(out.view(torch.uint8).cpu().numpy(), want):
             print(f"[rank {rank}] iter {it}: output mismatch", flush=True)
             failures += 1
+        if not np.allclose(O.decode(out32.view(torch.uint8).cpu().numpy(), dt), O.decode(want, dt), **tol):
+            print(f"[rank {rank}] iter {it}: fp32 (owner pre-reduced) output out of tolerance", flush=True)
+            failures += 1
         # disaggregated NCCL baseline: same activation bytes, outputs within bf16 tolerance
         bact, st = base.dispatch(x, idx)
         if not torch.equal(bact.view(torch.uint8), act[:rows].view(torch.uint8)):
@@ -91,7 +107,6 @@ def main() -> int:
             failures += 1
         bout = base.combine(bact, st, w.float())
         ref = torch.as_tensor(O.decode(want, dt), device=dev)
-        tol = dict(rtol=2.0**-8, atol=1e-3) if dt == "bf16" else dict(rtol=1e-5, atol=1e-6)
         if not torch.allclose(bout.float(), ref, **tol):
             print(f"[rank {rank}] iter {it}: baseline output out of tolerance", flush=True)
             failures += 1

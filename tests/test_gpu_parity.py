@@ -103,7 +103,11 @@ def _cluster_case(P, E, K, T_l, hidden, dtype, zipf, seed, max_tokens=None):
     return pkg, topo, pl, a, tb, payload
 
 
-def _run_cluster(pkg, topo, pl, a, tb, payload, dtype, acc, cl=None):
+def _run_cluster(pkg, topo, pl, a, tb, payload, dtype, acc, cl=None, w_at_dispatch=None):
+    """One emulated shuffle.  The router weights go to the dispatch too
+    (fs_dispatch_w) for fp32 accumulation by default, so the f32 results
+    cover the owner-side pre-reduction path wherever a token has >= 3 rows
+    (>= 2 for fp32 rows) on one remote owner."""
     from paper_2512_22036_b200.engine import EmulatedCluster, dtype_code
 
     P = topo.num_gpus
@@ -118,7 +122,9 @@ def _run_cluster(pkg, topo, pl, a, tb, payload, dtype, acc, cl=None):
          for i in ids]
     xs = [torch.as_tensor(payload[i], device=dev).contiguous() for i in ids]
     plans = cl.layout(idx)
-    cl.dispatch(xs, plans)
+    if w_at_dispatch is None:
+        w_at_dispatch = acc == "f32"
+    cl.dispatch(xs, plans, ws=w if w_at_dispatch else None)
     outs = [torch.empty((i.size, tb), dtype=torch.uint8, device=dev) for i in ids]
     cl.combine(plans, w, [o.view(tdt) for o in outs], dtype_code=code, acc=1 if acc == "f64" else 0)
     cl.check()
@@ -268,6 +274,41 @@ def test_push_rounds_parity(monkeypatch, P, E, K, T_l, hidden):
     for s in range(P):
         want = O.combine(acts, row_of, a.experts, a.weights, pl.owner, res["ids"][s], "bf16")
         assert np.array_equal(res["outs"][s], want), f"output/{s}"
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("P,E,K,T_l,hidden,zipf", [(2, 16, 8, 700, 1024, 0.0), (4, 64, 8, 300, 2048, 1.2),
+                                                    (8, 256, 8, 128, 7168, 1.2), (3, 12, 4, 257, 520, 0.5)])
+def test_owner_reduce_parity(monkeypatch, dtype, P, E, K, T_l, hidden, zipf):
+    """Owner-side pre-reduction (weights at dispatch, fp32 accumulate): within
+    the stated tolerance of the oracle and of the plain pull combine; the
+    activations stay bit-exact; weights at dispatch with f64 accumulation stay
+    bit-exact (no pre-reduction on that path)."""
+    monkeypatch.setenv("FUSCO_DISPATCH", "warp")
+    monkeypatch.setenv("FUSCO_COMBINE", "tma")
+    pkg, topo, pl, a, tb, payload = _cluster_case(P, E, K, T_l, hidden, dtype, zipf, seed=500 + P)
+    red = _run_cluster(pkg, topo, pl, a, tb, payload, dtype, "f32", w_at_dispatch=True)
+    plain = _run_cluster(pkg, topo, pl, a, tb, payload, dtype, "f32", w_at_dispatch=False)
+    exact = _run_cluster(pkg, topo, pl, a, tb, payload, dtype, "f64", w_at_dispatch=True)
+    layouts, row_of = _check_layout(red, a, pl, P)
+    acts = O.dispatch(payload, layouts)
+    tol = BF16_TOL if dtype == "bf16" else dict(rtol=1e-5, atol=1e-6)
+    mmin = 3 if dtype == "bf16" else 2
+    grouped = 0
+    for s in range(P):
+        ids = red["ids"][s]
+        owners = pl.owner[a.experts[ids]]
+        for g in range(P):
+            if g != s:
+                grouped += int(((owners == g).sum(axis=1) >= mmin).sum())
+        want_b = O.combine(acts, row_of, a.experts, a.weights, pl.owner, ids, dtype)
+        assert np.array_equal(exact["outs"][s], want_b), f"f64 output/{s} with weights at dispatch"
+        want = O.decode(want_b, dtype)
+        np.testing.assert_allclose(O.decode(red["outs"][s], dtype), want, **tol)
+        np.testing.assert_allclose(O.decode(red["outs"][s], dtype), O.decode(plain["outs"][s], dtype), **tol)
+    for g in range(P):
+        assert np.array_equal(red["acts"][g], acts[g]), f"activation/{g}"
+    assert grouped > 0, "the case must exercise pre-reduced groups"
 
 
 def test_engine_parity_fp32_payload(engines):

@@ -120,7 +120,7 @@ def test_library_exports_every_header_symbol():
     assert lib.fs_abi_version() == 2
 
 
-def test_library_validates_before_touching_cuda():
+def test_library_validates_before_touching_cuda(monkeypatch):
     """Argument errors come back as ValueError without needing a GPU."""
     from ctypes import byref, c_size_t, c_void_p
 
@@ -131,12 +131,18 @@ def test_library_validates_before_touching_cuda():
     # signal block + 2 parity copies of the epoch-tagged count words (u64 P x
     # (E + 1)) + the dispatch block words (u64 P x ceil(300 / 128)) + the
     # duplicate lists (int2 P x 300 x (K - 1)) + the activation rows + the
-    # expert-output rows
+    # expert-output rows + the owner pre-reduction records (80 B P x 300)
+    # and fp32 partials (P x 300 x 2 tb)
     a256 = lambda b: (b + 255) // 256 * 256  # noqa: E731
     fixed = 4096 + 2 * a256(8 * 257 * 8) + a256(8 * 3 * 8) + a256(8 * 300 * 7 * 8)
-    assert n.value == fixed + 2 * a256(1000 * 14336)
+    reduce = a256(8 * 300 * 80) + 8 * 300 * 2 * 14336
+    assert n.value == fixed + 2 * a256(1000 * 14336) + reduce
+    _lib.call("fs_region_bytes", 8, 256, 8, 14336, 300, 1000, 0, byref(n))
+    assert n.value == fixed + a256(1000 * 14336) + reduce
+    monkeypatch.setenv("FUSCO_OWNER_REDUCE", "0")  # no pre-reduction buffers
     _lib.call("fs_region_bytes", 8, 256, 8, 14336, 300, 1000, 0, byref(n))
     assert n.value == fixed + a256(1000 * 14336)
+    monkeypatch.delenv("FUSCO_OWNER_REDUCE")
     with pytest.raises(ValueError):
         _lib.call("fs_region_bytes", 0, 256, 8, 14336, 300, 1000, 1, byref(n))
     owner = (np.arange(8) % 2).astype(np.int32)
