@@ -137,7 +137,19 @@ def traffic(experts: np.ndarray, source: np.ndarray, owner: np.ndarray, P: int, 
     dups = rows - local_rows - primaries_in
     hbm_disp = T_l * tb + rows * tb + dups * tb
     hbm_comb = rows * tb + T_l * tb
-    return dict(d_eg=d_eg, d_in=d_in, c_eg=c_eg, c_in=c_in, rows=rows, hbm_disp=hbm_disp, hbm_comb=hbm_comb)
+    # with owner-side pre-reduction (bf16 rows, fp32 accumulate, K <= 8): a
+    # token's group of m >= 3 rows on one remote owner crosses as one fp32
+    # partial (2 tb) instead of m rows -- the bytes the combine actually pulls
+    c_eg_red = np.zeros(P)
+    c_in_red = np.zeros(P)
+    for g in range(P):
+        m = (own == g).sum(1)  # rows of each token on owner g
+        rem = source != g
+        b = np.where(m >= 3, 2 * tb, m * tb) * rem
+        c_eg_red[g] = b.sum()
+        c_in_red += np.bincount(source, weights=b, minlength=P)
+    return dict(d_eg=d_eg, d_in=d_in, c_eg=c_eg, c_in=c_in, rows=rows, hbm_disp=hbm_disp, hbm_comb=hbm_comb,
+                c_eg_red=c_eg_red, c_in_red=c_in_red)
 
 
 # ---------------------------------------------------------------------------
@@ -709,6 +721,12 @@ def main() -> int:
             "dispatch": float(tr["d_eg"].mean()) / (k_disp * 1e-3) / 1e9,
             "combine": float(tr["c_eg"].mean()) / (k_comb * 1e-3) / 1e9,
         },
+        # combine bytes that actually cross NVLink when owners pre-reduce
+        # (the algorithmic "combine" above counts every remote (t, k) row)
+        "combine_link_bytes_per_gpu": None if P == 1 else {
+            "algorithmic_rows": float(tr["c_eg"].mean()), "pulled_with_owner_reduce": float(tr["c_eg_red"].mean()),
+            "link_gbps_with_owner_reduce": float(tr["c_eg_red"].mean()) / (k_comb * 1e-3) / 1e9,
+        },
         "gbps_per_gpu": value / P,
         "roofline": roof,
         "nvlink_counters": nvlink,
@@ -716,8 +734,9 @@ def main() -> int:
         "launch_mode": "cuda_graph" if graph is not None else "eager",
         "dispatch_engine": args.dispatch if args.dispatch != "auto" else ("tma" if P == 1 else "warp"),
         "combine_engine": args.combine if args.combine != "auto" else ("warp" if P == 1 else "tma"),
-        "owner_reduce": bool(P > 1 and 2 <= K <= 8 and os.environ.get("FUSCO_OWNER_REDUCE", "1") != "0"
-                             and (args.combine in ("auto", "tma"))),
+        "owner_reduce": bool((3 if dtype == "bf16" else 2) <= K <= 8 and args.combine in ("auto", "tma")
+                             and os.environ.get("FUSCO_OWNER_REDUCE") != "0"
+                             and (os.environ.get("FUSCO_OWNER_REDUCE") == "1" or (P == 2 and T_l > 512))),
         "host_enqueue_ms_per_step": host_ms / args.steps,
         "clocks": clocks,
     }

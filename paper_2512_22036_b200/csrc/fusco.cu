@@ -127,7 +127,8 @@ struct fs_ctx {
   int push_warps;                  // warps per dispatch CTA that push before fanning out
   int claim_tokens;                // dispatch claim granularity: 1 = whole tokens, 0 = (token, slice) units
   int recs_written;                // this epoch's dispatch wrote pre-reduction records (fs_dispatch_w)
-  int owner_reduce_off;            // FUSCO_OWNER_REDUCE=0 at combine time (A/B)
+  int owner_reduce_off;            // no pre-reduction buffers (FUSCO_OWNER_REDUCE=0, or P = 1, K > 8)
+  int owner_reduce_force;          // FUSCO_OWNER_REDUCE=1: pre-reduce at every P and batch size
   int push_rounds;                 // FUSCO_PUSH_ROUNDS=1: per-CTA-round completion counts (A/B; default per unit)
   int fan_split;                   // FUSCO_FAN_SPLIT: -1 auto (by batch size), 0 rows, 1 slices
   int fan_poll;                    // FUSCO_FAN_POLL: 1 = per-CTA cached fan-out polling
@@ -451,6 +452,10 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
     h->dbg_relaxed = db && std::string(db) == "1";
     h->recs_written = 0;
     h->owner_reduce_off = !h->L.off_grp;
+    {
+      const char* orf = getenv("FUSCO_OWNER_REDUCE");
+      h->owner_reduce_force = orf && std::string(orf) == "1";
+    }
     const char* pr = getenv("FUSCO_PUSH_ROUNDS");
     h->push_rounds = pr && std::string(pr) == "1";
     const char* fsp = getenv("FUSCO_FAN_SPLIT");
@@ -793,7 +798,18 @@ int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes, const int32_t
   const bool bf = dtype == FS_DTYPE_BF16, f64 = acc == FS_ACC_F64;
   // owner-side pre-reduction: this epoch's dispatch wrote the records
   // (fs_dispatch_w), fp32 accumulation, the TMA engine (P > 1 default)
-  a.reduce = (h->combine_tma && vec16 && !f64 && h->world > 1 && h->recs_written && !h->owner_reduce_off) ? 1 : 0;
+  // (groups need >= 3 bf16 rows / >= 2 fp32 rows: with fewer experts per token there is nothing to reduce)
+  // Default (FUSCO_OWNER_REDUCE unset): P = 2 and more than kFanSplitTokens
+  // tokens, where it was measured faster (DeepSeek-V3 EP=2 step 412 vs 508 us,
+  // Zipf 422 vs 548, Qwen3 160 vs 185); at EP=4 it was neutral to slower
+  // (843 vs 850, Zipf 1018 vs 1078, Qwen3 299 vs 291) and at decode slower
+  // (the LOCAL-phase pass and grid barrier outweigh the bytes saved).
+  // FUSCO_OWNER_REDUCE=1 forces it on, =0 removes the buffers.  Ranks may
+  // decide differently (ragged batches): a source pulls an owner's partials
+  // only if that owner's mode word says it pre-reduced this epoch.
+  const bool red_auto = h->world == 2 && num_tokens > kFanSplitTokens;
+  a.reduce = (h->combine_tma && vec16 && !f64 && h->world > 1 && h->recs_written && !h->owner_reduce_off &&
+              h->K >= (bf ? 3 : 2) && (h->owner_reduce_force || red_auto)) ? 1 : 0;
   if (h->combine_tma && vec16) {
     fn = bf ? (f64 ? (const void*)combine_tma_kernel<true, true> : (const void*)combine_tma_kernel<true, false>)
             : (f64 ? (const void*)combine_tma_kernel<false, true> : (const void*)combine_tma_kernel<false, false>);

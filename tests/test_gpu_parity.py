@@ -286,6 +286,7 @@ def test_owner_reduce_parity(monkeypatch, dtype, P, E, K, T_l, hidden, zipf):
     bit-exact (no pre-reduction on that path)."""
     monkeypatch.setenv("FUSCO_DISPATCH", "warp")
     monkeypatch.setenv("FUSCO_COMBINE", "tma")
+    monkeypatch.setenv("FUSCO_OWNER_REDUCE", "1")  # at every world size and batch (default: P = 2, > 512 tokens)
     pkg, topo, pl, a, tb, payload = _cluster_case(P, E, K, T_l, hidden, dtype, zipf, seed=500 + P)
     red = _run_cluster(pkg, topo, pl, a, tb, payload, dtype, "f32", w_at_dispatch=True)
     plain = _run_cluster(pkg, topo, pl, a, tb, payload, dtype, "f32", w_at_dispatch=False)
