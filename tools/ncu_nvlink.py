@@ -54,7 +54,7 @@ def run(cfg: str, P: int, iters: int, seed: int) -> None:
         outs = [torch.empty_like(x) for x in xs]
         for _ in range(iters):
             plans = cl.layout(idx, with_masks=False)
-            cl.dispatch(xs, plans)
+            cl.dispatch(xs, plans, ws=ws)  # router weights at dispatch: owner pre-reduction where enabled
             cl.combine(plans, ws, outs, dtype_code=1 if dtype == "bf16" else 0)
         cl.check()
         for s in range(P):  # identity experts: the round trip returns x (weights sum to 1)
@@ -105,6 +105,7 @@ def summarize(cfg: str, P: int, path: str, seed: int) -> dict:
             row["alg_tx_bytes"] = float(tr["d_eg"][dev])   # deduplicated push to the other ranks
         if kern == "fs_combine" and phase == "remote":
             row["alg_rx_bytes"] = float(tr["c_in"][dev])   # rows pulled from the other ranks
+            row["alg_rx_bytes_owner_reduce"] = float(tr["c_in_red"][dev])  # with owner pre-reduction
         if row["us"] > 0 and row["nvl_tx_bytes"] is not None:
             row["nvl_tx_gbps"] = row["nvl_tx_bytes"] / (row["us"] * 1e-6) / 1e9
             row["nvl_rx_gbps"] = row["nvl_rx_bytes"] / (row["us"] * 1e-6) / 1e9
