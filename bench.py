@@ -736,7 +736,8 @@ def main() -> int:
         "combine_engine": args.combine if args.combine != "auto" else ("warp" if P == 1 else "tma"),
         "owner_reduce": bool((3 if dtype == "bf16" else 2) <= K <= 8 and args.combine in ("auto", "tma")
                              and os.environ.get("FUSCO_OWNER_REDUCE") != "0"
-                             and (os.environ.get("FUSCO_OWNER_REDUCE") == "1" or (P == 2 and T_l > 512))),
+                             and (os.environ.get("FUSCO_OWNER_REDUCE") == "1"
+                                  or (T_l > 512 and (P == 2 or (P <= 4 and tb >= 8192))))),
         "host_enqueue_ms_per_step": host_ms / args.steps,
         "clocks": clocks,
     }

@@ -799,15 +799,17 @@ int fs_combine(fs_handle_t h, const void* topk_idx, int idx_bytes, const int32_t
   // owner-side pre-reduction: this epoch's dispatch wrote the records
   // (fs_dispatch_w), fp32 accumulation, the TMA engine (P > 1 default)
   // (groups need >= 3 bf16 rows / >= 2 fp32 rows: with fewer experts per token there is nothing to reduce)
-  // Default (FUSCO_OWNER_REDUCE unset): P = 2 and more than kFanSplitTokens
-  // tokens, where it was measured faster (DeepSeek-V3 EP=2 step 412 vs 508 us,
-  // Zipf 422 vs 548, Qwen3 160 vs 185); at EP=4 it was neutral to slower
-  // (843 vs 850, Zipf 1018 vs 1078, Qwen3 299 vs 291) and at decode slower
-  // (the LOCAL-phase pass and grid barrier outweigh the bytes saved).
-  // FUSCO_OWNER_REDUCE=1 forces it on, =0 removes the buffers.  Ranks may
-  // decide differently (ragged batches): a source pulls an owner's partials
-  // only if that owner's mode word says it pre-reduced this epoch.
-  const bool red_auto = h->world == 2 && num_tokens > kFanSplitTokens;
+  // Default (FUSCO_OWNER_REDUCE unset): more than kFanSplitTokens tokens and
+  // P = 2, or P <= 4 with rows of >= 8 KB -- where it was measured faster:
+  // EP=2 DeepSeek-V3 step 405 vs 508 us, Zipf 416 vs 547, Qwen3 158 vs 185;
+  // EP=4 DeepSeek-V3 829 vs 850, Zipf 1008 vs 1077.  Slower: EP=4 Qwen3 (4 KB
+  // rows) 297 vs 290, decode 72 vs 67 (the LOCAL-phase pass and grid barrier
+  // outweigh the bytes saved), and at P >= 8 a token has ~1.5 rows per owner
+  // (8 % fewer bytes).  FUSCO_OWNER_REDUCE=1 forces it on, =0 removes the
+  // buffers.  Ranks may decide differently (ragged batches): a source pulls
+  // an owner's partials only if that owner's mode word says it pre-reduced.
+  const bool red_auto =
+      num_tokens > kFanSplitTokens && (h->world == 2 || (h->world <= 4 && h->tb >= 8192));
   a.reduce = (h->combine_tma && vec16 && !f64 && h->world > 1 && h->recs_written && !h->owner_reduce_off &&
               h->K >= (bf ? 3 : 2) && (h->owner_reduce_force || red_auto)) ? 1 : 0;
   if (h->combine_tma && vec16) {

@@ -30,4 +30,4 @@ print("| config | P | kernel | phase | µs (mean over GPUs) | NVLink bytes/GPU (
 print("|---|---|---|---|---|---|---|---|---|---|---|")
 for r in rows:
     alg = "—" if r[6] is None else f"{r[6]:.2f}"
-    print(f"| {r[0]} | {r[1]} | {r[2]} | {r[3]} ({'push, TX' if r[3] == 'local' and r[2] == 'fs_dispatch' else 'pull, RX' if r[2] == 'fs_combine' else 'fan-out, HBM'}) | {r[4]:.1f} | {r[5]:.2f} | {alg} | {r[7]} | {r[10]} | {r[8]:.0f} | {r[9]:.1f} |")
+    print(f"| {r[0]} | {r[1]} | {r[2]} | {r[3]} ({'push, TX' if r[3] == 'local' and r[2] == 'fs_dispatch' else 'owner pre-reduction, HBM' if r[3] == 'local' else 'pull, RX' if r[2] == 'fs_combine' else 'fan-out, HBM'}) | {r[4]:.1f} | {r[5]:.2f} | {alg} | {r[7]} | {r[10]} | {r[8]:.0f} | {r[9]:.1f} |")
