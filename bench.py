@@ -633,6 +633,11 @@ def main() -> int:
     routed = 2.0 * P * T_l * K * tb  # bytes per step, whole job
     value = routed / (ms * 1e-3) / 1e9
 
+    # the library's default for owner pre-reduction (fs_combine), reported on the line
+    owner_reduce = bool(P > 1 and (3 if dtype == "bf16" else 2) <= K <= 8 and args.combine in ("auto", "tma")
+                        and os.environ.get("FUSCO_OWNER_REDUCE") != "0"
+                        and (os.environ.get("FUSCO_OWNER_REDUCE") == "1"
+                             or (T_l > 512 and (P == 2 or (P <= 4 and tb >= 8192)))))
     pk = peaks()
     if P == 1:
         disp_b, comb_b = float(tr["hbm_disp"][0]), float(tr["hbm_comb"][0])
@@ -664,6 +669,13 @@ def main() -> int:
                 "frac": achieved / NVLINK_MEASURED, "peak_src": "measured peer copy 770 GB/s/dir (B200_PROFILING.md)",
                 "frac_of_nominal_900": achieved / NVLINK_NOMINAL,
                 "bytes_per_launch": b, "traffic": None}
+        if dom == "fs_combine" and owner_reduce:
+            # the bytes this combine actually moves (owner pre-reduction): the
+            # link's physical utilisation beside the reference-bytes figure
+            lb = float(np.maximum(tr["c_eg_red"], tr["c_in_red"]).max())
+            roof["link_bytes_per_launch"] = lb
+            roof["link_achieved"] = lb / (t * 1e-3) / 1e9
+            roof["link_frac"] = roof["link_achieved"] / NVLINK_MEASURED
     traffic_file = ROOT / "profiles" / "ncu_traffic.json"
     if traffic_file.exists() and P == 1:
         tf = json.loads(traffic_file.read_text())
@@ -734,10 +746,7 @@ def main() -> int:
         "launch_mode": "cuda_graph" if graph is not None else "eager",
         "dispatch_engine": args.dispatch if args.dispatch != "auto" else ("tma" if P == 1 else "warp"),
         "combine_engine": args.combine if args.combine != "auto" else ("warp" if P == 1 else "tma"),
-        "owner_reduce": bool((3 if dtype == "bf16" else 2) <= K <= 8 and args.combine in ("auto", "tma")
-                             and os.environ.get("FUSCO_OWNER_REDUCE") != "0"
-                             and (os.environ.get("FUSCO_OWNER_REDUCE") == "1"
-                                  or (T_l > 512 and (P == 2 or (P <= 4 and tb >= 8192))))),
+        "owner_reduce": owner_reduce,
         "host_enqueue_ms_per_step": host_ms / args.steps,
         "clocks": clocks,
     }

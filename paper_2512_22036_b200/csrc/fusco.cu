@@ -125,7 +125,6 @@ struct fs_ctx {
   unsigned long long* jcum_d;      // [P * nbmax] receiver fan-out schedule
   uint32_t* jorder_d;              // [P * nbmax]
   int push_warps;                  // warps per dispatch CTA that push before fanning out
-  int claim_tokens;                // dispatch claim granularity: 1 = whole tokens, 0 = (token, slice) units
   int recs_written;                // this epoch's dispatch wrote pre-reduction records (fs_dispatch_w)
   int owner_reduce_off;            // no pre-reduction buffers (FUSCO_OWNER_REDUCE=0, or P = 1, K > 8)
   int owner_reduce_force;          // FUSCO_OWNER_REDUCE=1: pre-reduce at every P and batch size
@@ -172,7 +171,6 @@ FsArgs make_args(const fs_ctx* h, int T, int idx64) {
   a.nbmax = h->L.nbmax;
   a.dupq_cap = h->L.dupq_cap;
   a.push_warps = h->push_warps;
-  a.claim_tokens = h->claim_tokens;
   a.dbg_relaxed = h->dbg_relaxed;
   a.fan_poll = h->fan_poll;
   a.push_rounds = h->push_rounds;
@@ -446,8 +444,6 @@ int fs_create(int device, int rank, int world, int num_experts, int topk, int to
     // fan out duplicates from the start): FUSCO_PUSH_WARPS, default all
     const char* pw = getenv("FUSCO_PUSH_WARPS");
     h->push_warps = pw ? std::max(1, std::min(kMoveThreads / 32, atoi(pw))) : kMoveThreads / 32;
-    const char* cl = getenv("FUSCO_CLAIM");  // unit | token
-    h->claim_tokens = cl && std::string(cl) == "token";
     const char* db = getenv("FUSCO_DBG_BLK");
     h->dbg_relaxed = db && std::string(db) == "1";
     h->recs_written = 0;

@@ -88,7 +88,6 @@ struct FsArgs {
   int nbmax;                 // completion blocks per source (ceil(max_tokens / blk))
   long long dupq_cap;        // duplicate-list entries per source in a region (max_tokens * (K - 1))
   int push_warps;            // warps per CTA that push first (the rest fan out from the start)
-  int claim_tokens;          // 1: pushers claim whole tokens (all slices), 0: (token, slice) units
   int dbg_relaxed;           // timing experiments only: block counts without release ordering
   // owner-side pre-reduction (0 in every field when the handle has no partial buffers)
   size_t off_grp, off_part;  // region offsets: GrpRec[P][max_tokens], fp32 partials [P][max_tokens][2 * tb]
