@@ -108,8 +108,11 @@ def test_full_size_matches_reference_digests(name):
 
 
 FULL = [
-    # P, E, K, T_l, hidden, zipf, expert
+    # P, E, K, T_l, hidden, zipf, expert (expert "scaled+reduce": owner pre-reduction forced on)
     pytest.param(8, 256, 8, 4096, 7168, 0.0, "scaled", id="dsv3-ep8"),
+    pytest.param(8, 256, 8, 4096, 7168, 1.2, "scaled+reduce", id="dsv3-zipf-ep8-reduce"),
+    pytest.param(2, 256, 8, 4096, 7168, 0.0, "scaled", id="dsv3-ep2"),          # pre-reduction by default
+    pytest.param(4, 256, 8, 4096, 7168, 1.2, "identity", id="dsv3-zipf-ep4"),   # pre-reduction by default
     pytest.param(8, 256, 8, 4096, 7168, 1.2, "identity", id="dsv3-zipf-ep8"),
     pytest.param(1, 256, 8, 4096, 7168, 1.2, "identity", id="dsv3-zipf-p1"),
     pytest.param(8, 256, 8, 128, 7168, 0.0, "scaled", id="dsv3-decode-ep8"),
@@ -128,8 +131,12 @@ def _scaled_gpu(act_bf16: torch.Tensor, e: torch.Tensor) -> torch.Tensor:
 
 
 @pytest.mark.parametrize("P,E,K,T_l,hidden,zipf,expert", FULL)
-def test_full_size_bf16_against_oracle(P, E, K, T_l, hidden, zipf, expert):
+def test_full_size_bf16_against_oracle(monkeypatch, P, E, K, T_l, hidden, zipf, expert):
     from paper_2512_22036_b200.engine import EmulatedCluster
+
+    if expert.endswith("+reduce"):
+        monkeypatch.setenv("FUSCO_OWNER_REDUCE", "1")
+        expert = expert.split("+")[0]
 
     pkg = _pkg()
     topo = pkg.box(P)
@@ -148,15 +155,17 @@ def test_full_size_bf16_against_oracle(P, E, K, T_l, hidden, zipf, expert):
 
         def run(acc):
             plans = cl.layout(idx)
-            cl.dispatch(xs, plans)
+            wdt = torch.float64 if acc == "f64" else torch.float32
+            ws = [torch.as_tensor(a.weights[i], dtype=wdt, device=dev) for i in ids]
+            # the router weights reach the dispatch (owner pre-reduction for the
+            # fp32 combine where the library enables it; never for f64)
+            cl.dispatch(xs, plans, ws=ws)
             if scaled:
                 for r, p in zip(cl.ranks, plans):
                     n = p.num_rows
                     e = torch.repeat_interleave(torch.as_tensor(r.local_experts, device=dev),
                                                 p.expert_counts.to(torch.int64))
                     r.act_out(n, torch.bfloat16).copy_(_scaled_gpu(r.act(n, torch.bfloat16), e))
-            wdt = torch.float64 if acc == "f64" else torch.float32
-            ws = [torch.as_tensor(a.weights[i], dtype=wdt, device=dev) for i in ids]
             outs = [torch.empty((i.size, hidden), dtype=torch.bfloat16, device=dev) for i in ids]
             cl.combine(plans, ws, outs, dtype_code=1, src=src, acc=1 if acc == "f64" else 0)
             cl.check()

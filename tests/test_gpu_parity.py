@@ -312,6 +312,48 @@ def test_owner_reduce_parity(monkeypatch, dtype, P, E, K, T_l, hidden, zipf):
     assert grouped > 0, "the case must exercise pre-reduced groups"
 
 
+def test_owner_reduce_ragged_mixed_decisions(monkeypatch):
+    """P = 2 with 700 tokens on rank 0 and 300 on rank 1: by default only
+    rank 0 pre-reduces as an owner (> 512 tokens), rank 1 does not; each
+    source pulls partials only from owners whose mode word says so.  Both
+    outputs within tolerance, activations bit-exact, over two epochs."""
+    from paper_2512_22036_b200.engine import EmulatedCluster
+
+    monkeypatch.setenv("FUSCO_DISPATCH", "warp")
+    monkeypatch.setenv("FUSCO_COMBINE", "tma")
+    monkeypatch.delenv("FUSCO_OWNER_REDUCE", raising=False)
+    P, E, K, hidden = 2, 16, 8, 1024
+    pkg = _pkg()
+    topo = pkg.box(P)
+    pl = pkg.round_robin_placement(E, topo)
+    a = pkg.gen_realworld(P * 700, K, topo, pl, seed=91, zipf_s=0.3)
+    ids = [np.flatnonzero(a.source == 0)[:700], np.flatnonzero(a.source == 1)[:300]]
+    sel = np.sort(np.concatenate(ids))
+    experts, weights, source = a.experts[sel], a.weights[sel], a.source[sel]
+    loc = [np.flatnonzero(source == s) for s in range(P)]
+    tb = hidden * 2
+    vals = np.random.default_rng(5).standard_normal((sel.size, hidden)).astype(np.float32)
+    payload = O.encode(vals, "bf16")
+    layouts, row_of = O.activation_layouts(experts, source, pl.owner, P)
+    acts = O.dispatch(payload, layouts)
+    with EmulatedCluster(P, E, K, tb, 700, owner=pl.owner) as cl:
+        dev = cl.device
+        idx = [torch.as_tensor(experts[i], device=dev) for i in loc]
+        xs = [torch.as_tensor(payload[i], device=dev).contiguous() for i in loc]
+        ws = [torch.as_tensor(weights[i], dtype=torch.float32, device=dev) for i in loc]
+        for _ in range(2):
+            plans = cl.layout(idx)
+            cl.dispatch(xs, plans, ws=ws)
+            outs = [torch.empty((i.size, tb), dtype=torch.uint8, device=dev) for i in loc]
+            cl.combine(plans, ws, [o.view(torch.bfloat16) for o in outs], dtype_code=1, acc=0)
+            cl.check()
+            for g in range(P):
+                assert np.array_equal(cl.ranks[g].act(plans[g].num_rows).cpu().numpy(), acts[g])
+            for s_ in range(P):
+                want = O.decode(O.combine(acts, row_of, experts, weights, pl.owner, loc[s_], "bf16"), "bf16")
+                np.testing.assert_allclose(O.decode(outs[s_].cpu().numpy(), "bf16"), want, **BF16_TOL)
+
+
 def test_engine_parity_fp32_payload(engines):
     """fp32 rows (the reference's own payload dtype) through both engines."""
     pkg, topo, pl, a, tb, payload = _cluster_case(4, 32, 4, 300, 1024, "f32", 0.7, seed=9)
