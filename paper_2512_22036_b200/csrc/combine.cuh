@@ -536,7 +536,9 @@ __global__ void __launch_bounds__(kCombThreads, 3)  // 3 CTAs/SM (the stage budg
                  : (Acc)reinterpret_cast<const float*>(topk_w)[pos];
     };
     // balancer on: items claimed dynamically; off: static striding over the CTAs
-    const bool dyn = a.balance != 0;
+    // (static striding also when there are no more items than producers x 2:
+    // decode batches, where every claim would be one more serialised atomic)
+    const bool dyn = a.balance != 0 && items > 2LL * gridDim.x;
     long long u = dyn ? claim_warp(ctr) : (long long)blockIdx.x;
     KMeta m = u < items ? load_meta(a, idx, row_of, (int)((uint32_t)u / (uint32_t)S), lane) : KMeta{0, 0};
     Acc wl = u < items ? load_w(u) : (Acc)0;

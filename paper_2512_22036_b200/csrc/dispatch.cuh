@@ -226,7 +226,11 @@ __device__ void fan_work(const FsArgs& a, uint32_t epoch, size_t act_off, int nv
   const unsigned long long nwk = (unsigned long long)gridDim.x * warps_per_cta;
   unsigned long long grp = wid;
   for (;; grp += nwk) {
-    const unsigned long long g0 = (a.balance ? (unsigned long long)claim_warp(ctr) : grp) * kFanGroup;
+    // small batches (a.fan_split: uniform 4 KB slice units, fewer than the
+    // warps) stride statically: a claim atomic per group would serialise
+    // ~1.5k claims on one address behind the block's arrival
+    const unsigned long long g0 =
+        ((a.balance && !a.fan_split) ? (unsigned long long)claim_warp(ctr) : grp) * kFanGroup;
     for (int gi = 0; gi < kFanGroup; ++gi) {
       const unsigned long long u = g0 + gi;
       // wait until the published prefix covers u (or every job is in)
