@@ -14,11 +14,11 @@ namespace cg = cooperative_groups;
 // of the warp holds (owner g_k, row r_k) of the token's k-th expert.  Per
 // destination rank only the first k crosses NVLink (the per-rank dedup of
 // routing.py:94-97 / planner.py:231 with one GPU per "node"); for the own
-// rank every k is written directly from registers.  The sender records, for
-// each destination row, the row holding its bytes (fan_src): itself, or the
-// primary row of the same token on that rank.  After every source's CTAs
-// have signalled arrival, the receiver copies primary -> duplicate rows in
-// its own HBM.  The activation buffer is single: a rank's next dispatch
+// rank every k is written directly from registers.  A token's further rows
+// on an already-reached rank are listed (duplicate row, primary row) in that
+// rank's duplicate list for the token's completion block; as each block of
+// each source lands, the receiver copies primary -> duplicate rows in its
+// own HBM (fan_watch / fan_work).  The activation buffer is single: a rank's next dispatch
 // cannot start before every peer published its next-epoch counts, i.e.
 // finished pulling this epoch's rows in combine (fusco.cu region_layout).
 // ===========================================================================

@@ -74,7 +74,8 @@ struct FsArgs {
   // Iteration counter in device memory (per handle), so a captured CUDA graph
   // replays correctly: fs_layout's LOCAL phase uses *epoch + 1 and stores it;
   // every later phase/kernel of the iteration reads it.  parity = epoch & 1
-  // selects the act / count / fan_src copy.
+  // selects the count-matrix copy and the per-epoch scratch (work counters,
+  // block accounting).
   uint32_t* epoch_ptr;
   long long max_rows;
   const int32_t* owner;      // [E] expert -> rank
