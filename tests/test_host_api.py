@@ -416,3 +416,31 @@ def test_bench_traffic_matches_reference_volumes(cfg, P, want):
            tr["c_eg"].mean() / M, np.maximum(tr["c_eg"], tr["c_in"]).max() / M)
     assert np.allclose(got, want, atol=0.051), got
     assert np.array_equal(tr["d_eg"], O.dispatch_loads(a.experts, a.source, pl.owner, P, tb, 1))
+
+
+@pytest.mark.parametrize("cfg,P", [("dsv3", 2), ("dsv3_zipf", 4), ("qwen3", 2), ("dsv3_decode", 2)])
+def test_bench_traffic_owner_reduced_bytes(cfg, P):
+    """The combine bytes with owner-side pre-reduction (bench.traffic's
+    c_eg_red / c_in_red, the figure ncu's NVLink counters matched): per
+    (token, remote owner) group of m rows, one fp32 partial (2 tb) when
+    m >= 3, else the m rows -- brute force over the routing."""
+    import bench
+
+    hidden, dtype, E, K, T_l, _, _ = bench.CONFIGS[cfg]
+    a, pl = bench.routing_for(cfg, P, 0)
+    tb = hidden * 2
+    tr = bench.traffic(a.experts, a.source, pl.owner, P, tb, T_l)
+    own = pl.owner[a.experts]
+    eg = np.zeros(P)
+    ing = np.zeros(P)
+    for t in range(a.num_tokens):
+        s = a.source[t]
+        for g in range(P):
+            m = int((own[t] == g).sum())
+            if g == s or m == 0:
+                continue
+            b = 2 * tb if m >= 3 else m * tb
+            eg[g] += b
+            ing[s] += b
+    assert np.array_equal(tr["c_eg_red"], eg) and np.array_equal(tr["c_in_red"], ing)
+    assert (tr["c_eg_red"] <= tr["c_eg"]).all()
