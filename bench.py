@@ -680,6 +680,20 @@ def main() -> int:
     if traffic_file.exists() and P == 1:
         tf = json.loads(traffic_file.read_text())
         roof["traffic"] = tf.get(f"{args.config}/n{P}/{dom}")
+    nvl_file = ROOT / "profiles" / f"r2_nvl_counters_{args.config}_ep{P}.json"
+    if P > 1 and nvl_file.exists():
+        # ncu counters of the same kernel on P real GPUs (tools/ncu_nvlink.py, phased
+        # run): DRAM bytes per launch and the NVLink bytes it moved (push TX / pull RX)
+        try:
+            ks = [k for k in json.loads(nvl_file.read_text())["kernels"]
+                  if k["kernel"] == dom and k["phase"] == ("local" if dom == "fs_dispatch" else "remote")]
+            if ks:
+                roof["traffic"] = float(np.mean([k["dram_bytes"] for k in ks]))
+                roof["nvlink_counter_bytes"] = float(np.max([k["nvl_tx_bytes" if dom == "fs_dispatch"
+                                                               else "nvl_rx_bytes"] for k in ks]))
+                roof["counters_src"] = f"profiles/{nvl_file.name} (ncu, owner pre-reduction as in that run)"
+        except (OSError, KeyError, ValueError):
+            pass
     nvlink = None
     if links is not None and (links >= 0).all():
         # measured link bytes per step and GPU against the algorithmic bytes
