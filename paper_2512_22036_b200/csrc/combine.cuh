@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(kMoveThreads)
 template <bool BF16>
 __device__ void owner_prereduce(const FsArgs& a, uint32_t epoch, size_t src_off, int mmin) {
   using EL = Elem<int4, BF16>;
-  constexpr int kCh = 2;  // 16-byte column chunks per lane per item (loads in flight)
+  constexpr int kCh = 2;  // 16-byte column chunks per lane per item (loaded together below)
   const int P = a.world, s = a.rank, K = a.K, tb = a.tb, nv = tb / 16;
   const int lane = threadIdx.x & 31;
   const int par = (int)(epoch & 1u);
@@ -380,17 +380,19 @@ __device__ void owner_prereduce(const FsArgs& a, uint32_t epoch, size_t src_off,
     const int t = gt - (__shfl_sync(kFull, incl, q) - __shfl_sync(kFull, tq, q));
     const long long slot = (long long)q * a.max_tokens + t;
     const GrpRec* rec = recs + slot;
+    // the whole record in one round trip: every lane the header, lane k < K
+    // its row and weight (used only where the k-mask has the bit)
     const uint32_t e = __ldcg(&rec->epoch), km = __ldcg(&rec->kmask);
-    if (e != epoch || __popc(km) < mmin) continue;
     int rk = 0;
     float wk = 0.f;
-    if (lane < K && ((km >> lane) & 1u)) {
+    if (lane < K) {
       rk = __ldcg(&rec->rows[lane]);
       wk = __ldcg(&rec->w[lane]);
-      if (rk < 0 || rk >= a.max_rows) {
-        record_error(a.status, FS_ERANGE, kSiteRows);
-        rk = 0;
-      }
+    }
+    if (e != epoch || __popc(km) < mmin) continue;
+    if (lane < K && ((km >> lane) & 1u) && (rk < 0 || rk >= a.max_rows)) {
+      record_error(a.status, FS_ERANGE, kSiteRows);
+      rk = 0;
     }
     int rr[kGrpMaxK];
     float ww[kGrpMaxK];
@@ -400,28 +402,44 @@ __device__ void owner_prereduce(const FsArgs& a, uint32_t epoch, size_t src_off,
       ww[k] = __shfl_sync(kFull, wk, k);
     }
     char* dst = part + (size_t)slot * 2 * tb;
-    const int v_end = min(nv, (pc + 1) * cols_per_part);
-    for (int v = pc * cols_per_part + lane; v < v_end; v += 32) {
-      float acc[EL::N];
+    // the part's two chunks per lane: both chunks' loads of four rows in
+    // flight together (a group rarely has more than four rows)
+    const int va = pc * 32 * kCh + lane, vb = va + 32;
+    const bool ha = va < nv, hb = vb < nv;
+    float acc_a[EL::N], acc_b[EL::N];
 #pragma unroll
-      for (int e2 = 0; e2 < EL::N; ++e2) acc[e2] = 0.f;
+    for (int e2 = 0; e2 < EL::N; ++e2) acc_a[e2] = acc_b[e2] = 0.f;
 #pragma unroll
-      for (int k0 = 0; k0 < kGrpMaxK; k0 += 4) {  // four rows' loads in flight, k ascending
-        int4 x[4];
+    for (int k0 = 0; k0 < kGrpMaxK; k0 += 4) {
+      if (k0 > 0 && (km >> k0) == 0u) break;
+      int4 xa[4], xb[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int k = k0 + j;
-          if (k < K && ((km >> k) & 1u)) x[j] = ld_nc(reinterpret_cast<const int4*>(src + (size_t)rr[k] * tb) + v);
+      for (int j = 0; j < 4; ++j) {
+        const int k = k0 + j;
+        xa[j] = xb[j] = make_int4(0, 0, 0, 0);
+        if (k < K && ((km >> k) & 1u)) {
+          const int4* row = reinterpret_cast<const int4*>(src + (size_t)rr[k] * tb);
+          if (ha) xa[j] = ld_nc(row + va);
+          if (hb) xb[j] = ld_nc(row + vb);
         }
+      }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int k = k0 + j;
-          if (k < K && ((km >> k) & 1u)) {
+      for (int j = 0; j < 4; ++j) {
+        const int k = k0 + j;
+        if (k < K && ((km >> k) & 1u)) {
 #pragma unroll
-            for (int e2 = 0; e2 < EL::N; ++e2) acc[e2] = __fmaf_rn(ww[k], EL::get(x[j], e2), acc[e2]);
+          for (int e2 = 0; e2 < EL::N; ++e2) {
+            acc_a[e2] = __fmaf_rn(ww[k], EL::get(xa[j], e2), acc_a[e2]);
+            acc_b[e2] = __fmaf_rn(ww[k], EL::get(xb[j], e2), acc_b[e2]);
           }
         }
       }
+    }
+#pragma unroll
+    for (int c = 0; c < kCh; ++c) {
+      const int v = c ? vb : va;
+      if (!(c ? hb : ha)) break;
+      const float* acc = c ? acc_b : acc_a;
       int4* o = reinterpret_cast<int4*>(dst) + (size_t)v * (EL::N / 4);
 #pragma unroll
       for (int h = 0; h < EL::N / 4; ++h)
